@@ -1,0 +1,416 @@
+"""Benchmark of the batched split-format DFT (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config NAME] [--impl ours|reference]
+
+A step is one pass of the hot path -- one batched forward transform of the
+whole config batch (one kernel launch for N <= 4096) -- over inputs already
+resident in HBM.  Default workload: BASELINE.json configs[1] (N=64 fp32,
+B=2^20, seed 1, standard normal).  Under torchrun each rank transforms its
+own B-row batch on its own GPU (weak scaling, no collective on the data
+path); the timed region is bracketed by barrier + synchronize, timed with
+CUDA events on the launching stream, and the max over ranks is reported.
+
+Rank 0 prints ONE JSON line with the driver contract keys plus
+``roofline`` (HBM-bound: algorithmic bytes 4*N*sizeof(real) per transform /
+the measured kernel duration, against MEASURED_PEAKS.json hbm_gbs),
+``cpu_baseline`` (the oracle's numpy restatement of the reference executor,
+timed on this host's cores on a bounded sample of the same workload),
+``e2e`` (the same metric through the public ``fft_split`` on pinned HOST
+buffers, H2D + D2H inside the timed region), ``gpu_launches`` and
+``clocks`` (NVML samples taken during the timed region).
+
+``--impl reference`` times the reference algorithm's CPU implementation
+(the oracle's numpy port of transform.py, all host cores) on the same
+config and prints the same line with ``"impl": "reference"``.
+"""
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads  # noqa: E402
+
+BASELINE_METRIC = "batched split-DFT transforms/s and achieved HBM GB/s vs peak at 1/2/4/8 B200"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2_n64_f32", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--algorithm", default="dit", choices=["dit", "dif"])
+    ap.add_argument("--radix-log", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0,
+                    help="target CPU time of the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(cfg_name):
+    """dram bytes per launch from the committed ncu --set full capture, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        d = json.load(f)
+    v = d.get(cfg_name)
+    return None if v is None else float(v["dram_bytes_per_launch"])
+
+
+# ---------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """NVML SM clock + clock-event reasons sampled every ~5 ms in a thread."""
+
+    REASONS = {
+        "hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+        "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+        "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+        "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+        "hw_power_brake_slowdown": "nvmlClocksEventReasonHwPowerBrakeSlowdown",
+        "gpu_idle": "nvmlClocksEventReasonGpuIdle",
+        "applications_clocks_setting": "nvmlClocksEventReasonApplicationsClocksSetting",
+        "sync_boost": "nvmlClocksEventReasonSyncBoost",
+    }
+
+    def __init__(self, torch_device):
+        self.samples = []
+        self.ok = False
+        self._stop = threading.Event()
+        self.window = None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            idx = torch.cuda._get_nvml_device_index(torch_device)
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # NVML missing: report it instead of guessing
+            self.err = repr(e)
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def stop(self):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": f"nvml unavailable: {self.err}"}
+        t0, t1 = self.window
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        note = "samples inside the timed region"
+        if not inside:   # region shorter than one sample period: nearest samples
+            inside = sorted(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))[:3]
+            note = "timed region shorter than the 5 ms sampling period; nearest samples"
+        mask = 0
+        for s in inside:
+            mask |= s[2]
+        reasons = [k for k, attr in self.REASONS.items() if mask & getattr(self.nv, attr, 0)]
+        return {"sm_mhz": float(np.median([s[1] for s in inside])) if inside else None,
+                "sm_max_mhz": float(self.max_mhz), "reasons": reasons,
+                "samples": len(inside), "note": note}
+
+
+# ------------------------------------------------------------ CPU side ---
+def _cpu_worker(args):
+    cfg_name, rows, algorithm = args
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    sys.path.insert(0, ROOT)
+    from oracle import oracle
+    cfg = workloads.CONFIGS[cfg_name]
+    re, im = workloads.generate(cfg, rows=rows)
+    plan = oracle.NumpyPlan(cfg.log2n, algorithm)
+    t0 = time.perf_counter()
+    for b in range(rows):
+        oracle.split_to_split_numpy(plan, re[b], im[b])
+    return time.perf_counter() - t0
+
+
+def cpu_port_rate(cfg, algorithm, target_s, procs=None):
+    """Transforms/s of the numpy port of the reference executor over all host
+    cores (one process per core, the reference has no internal parallelism).
+    Sample: every worker transforms the first r rows of the config stream,
+    with r sized so that one worker computes for about target_s seconds."""
+    import multiprocessing as mp
+    procs = procs or os.cpu_count() or 1
+    # size the sample with a 1-process probe
+    probe_rows = max(1, min(cfg.batch, 64 if cfg.log2n <= 12 else 1))
+    t = _cpu_worker((cfg.name, probe_rows, algorithm))
+    per_row = t / probe_rows
+    rows = int(max(1, min(cfg.batch, target_s / max(per_row, 1e-9))))
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        times = pool.map(_cpu_worker, [(cfg.name, rows, algorithm)] * procs)
+    rate = rows * procs / max(times)
+    sample = (f"first {rows} rows of the {cfg.name} stream in each of {procs} worker processes "
+              f"(SplitSignal -> interleave -> fft -> deinterleave per row, numpy port of "
+              f"transform.py:123-270); throughput = rows / max worker time")
+    return rate, procs, sample, per_row
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------ reference ---
+def run_reference(args):
+    world, rank, _ = dist_env()
+    cfg = workloads.CONFIGS[args.config]
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    per_step_target = 1.0
+    rate, procs, sample, per_row = cpu_port_rate(cfg, args.algorithm, min(2.0, per_step_target), procs)
+    # steps: each a bounded sample (the same row prefix) on all cores
+    import multiprocessing as mp
+    rows = int(max(1, min(cfg.batch, per_step_target / max(per_row, 1e-9))))
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        for _ in range(args.warmup):
+            pool.map(_cpu_worker, [(cfg.name, rows, args.algorithm)] * procs)
+        t_steps = []
+        for _ in range(args.steps):
+            t_steps.append(max(pool.map(_cpu_worker, [(cfg.name, rows, args.algorithm)] * procs)))
+    ms = 1e3 * float(np.mean(t_steps))
+    value = rows * procs / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": BASELINE_METRIC, "value": value, "unit": "transforms/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "n": cfg.n, "batch": cfg.batch, "input_dtype": cfg.dtype,
+                   "seed": cfg.seed, "step_rows": rows * procs},
+        "cpu_baseline": {"value": value, "unit": "transforms/s", "cores": procs, "kind": "port",
+                         "sample": f"each step: {sample.replace(f'first {rows}', f'first {rows}')}",
+                         "cpu_model": cpu_model()},
+        "e2e": {"value": value, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours ---
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
+    torch.cuda.set_device(device)
+
+    import paper_2504_07264_b200 as sf
+    from paper_2504_07264_b200 import _ffi
+
+    cfg = workloads.CONFIGS[args.config]
+    dt = torch.float32 if cfg.dtype == "f32" else torch.float64
+    # this rank's batch: rank 0 = the config's canonical stream; others a
+    # seeded variant of the same distribution (weak scaling: B rows per GPU)
+    if rank == 0:
+        re, im = workloads.generate(cfg)
+    else:
+        c2 = workloads.Config(cfg.name, cfg.log2n, cfg.batch, cfg.dtype, cfg.seed * 1000 + rank, cfg.dist)
+        re, im = workloads.generate(c2)
+    x_re = torch.from_numpy(re).to(device)
+    x_im = torch.from_numpy(im).to(device)
+    del re, im
+    y_re = torch.empty_like(x_re)
+    y_im = torch.empty_like(x_im)
+    plan = sf.make_plan(cfg.log2n, args.algorithm, dtype=dt, device=device, radix_log=args.radix_log)
+    stream = torch.cuda.current_stream(device)
+    ws_bytes = plan.workspace_bytes(cfg.batch)
+    ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
+    sp = stream.cuda_stream
+    b, n = cfg.batch, cfg.n
+
+    def step():
+        _ffi.check(_ffi.lib.sfft_exec_split(plan._handle, x_re.data_ptr(), x_im.data_ptr(),
+                                            y_re.data_ptr(), y_im.data_ptr(), b, n, n,
+                                            _ffi.SFFT_FORWARD, ws.data_ptr() if ws_bytes else None, sp))
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(device)
+
+    clocks = ClockSampler(device)
+    clocks.start()
+    time.sleep(0.02)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(device)
+    launches0 = _ffi.launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    t_wall0 = time.perf_counter()
+    ev[0].record(stream)
+    for k in range(args.steps):
+        step()
+        ev[k + 1].record(stream)
+    torch.cuda.synchronize(device)
+    t_wall1 = time.perf_counter()
+    if world > 1:
+        dist.barrier()
+    launches = _ffi.launch_count() - launches0
+    clocks.mark(t_wall0, t_wall1)
+    time.sleep(0.01)
+    clocks.stop()
+    per_step = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    total_ms = ev[0].elapsed_time(ev[-1])
+    ms_local = total_ms / args.steps
+    kern_local = float(np.mean(per_step)) / plan.launches_per_exec
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms = max_over_ranks(ms_local)
+    kern_ms = max_over_ranks(kern_local)
+    value = world * b / (ms / 1e3)
+
+    # ---------------- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hr = torch.empty((b, n), dtype=dt, pin_memory=True)
+        hi = torch.empty((b, n), dtype=dt, pin_memory=True)
+        hr.copy_(x_re)
+        hi.copy_(x_im)
+        ho_r = torch.empty((b, n), dtype=dt, pin_memory=True)
+        ho_i = torch.empty((b, n), dtype=dt, pin_memory=True)
+        sf.fft_split(hr, hi, out=(ho_r, ho_i), plan=plan)   # warm the allocator
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(device)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            sf.fft_split(hr, hi, out=(ho_r, ho_i), plan=plan)
+        e1.record(stream)
+        torch.cuda.synchronize(device)
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps)
+        ok = torch.equal(ho_r.to(device), y_re) and torch.equal(ho_i.to(device), y_im)
+        e2e = {"value": world * b / (e2e_ms / 1e3), "unit": "transforms/s",
+               "h2d_bytes_per_step": int(hr.numel() * hr.element_size() * 2),
+               "d2h_bytes_per_step": int(ho_r.numel() * ho_r.element_size() * 2),
+               "ms_per_step": e2e_ms, "api": "paper_2504_07264_b200.fft_split(host pinned re, im, out=host)",
+               "matches_device_result": bool(ok)}
+        del hr, hi, ho_r, ho_i
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    bytes_per_launch = 4 * n * cfg.elem_bytes * b / plan.launches_per_exec
+    achieved = 4 * n * cfg.elem_bytes * b / (kern_ms * plan.launches_per_exec / 1e3) / 1e9
+    traffic = ncu_traffic(cfg.name)
+    line = {
+        "metric": BASELINE_METRIC,
+        "value": value,
+        "unit": "transforms/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if cfg.dtype == "f32" else "f64",
+        "data": "synthetic (seeded, BASELINE.json config shapes/distributions; workloads.py)",
+        "config": {"workload": cfg.name, "n": n, "batch_per_gpu": b, "global_batch": b * world,
+                   "input_dtype": cfg.dtype, "seed": cfg.seed, "algorithm": args.algorithm,
+                   "radix_log": plan.radix_log, "parallelism": f"batch-sharded x{world}, no collective",
+                   "l2": f"inputs {2 * n * cfg.elem_bytes * b / 2**20:.0f} MiB > 126 MB L2 (no flush needed)"},
+        "gbs_algorithmic": 4 * n * cfg.elem_bytes * b * world / (ms / 1e3) / 1e9,
+        "gflops_5nlogn": 5 * n * cfg.log2n * b * world / (ms / 1e3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": f"sfft_fused_kernel<{cfg.dtype},{cfg.log2n}>" if cfg.log2n <= 12 else "sfft_pass_kernel",
+                     "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "kernel_ms": kern_ms, "peak_source": peak_src,
+                     "frac_of_datasheet_8tbs": achieved / 8000.0},
+        "gpu_launches": int(launches),
+        "clocks": clocks.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline and world == 1:
+        rate, procs, sample, _ = cpu_port_rate(cfg, args.algorithm, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rate, "unit": "transforms/s", "cores": procs, "kind": "port",
+                                "sample": sample, "cpu_model": cpu_model()}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,130 @@
+/*
+ * splitfft_b200.h -- C ABI of the B200-native split-format DFT.
+ *
+ * The reference (`splitfft`, pure Python/NumPy) has no FFI: its boundary is
+ * the Python operator API in pkg/src/splitfft/__init__.py:14-55.  Each entry
+ * point below replaces one piece of that API so that a ctypes / cffi / cgo
+ * binding can drive the GPU path with plain pointers and sizes
+ * (INTEGRATION.md shows the bindings).  No torch types cross this boundary.
+ *
+ * Conventions
+ *   - Every call returns an int status: SFFT_OK (0) or an SFFT_E* code.
+ *     sfft_last_error() returns a thread-local message for the last failure.
+ *     Python maps 1 -> ValueError, 2 -> CapacityError, 3 -> RuntimeError,
+ *     mirroring the reference's exception types (transform.py:72-76,
+ *     errors.py:4-5).
+ *   - Plans are immutable after creation and may be shared by host threads;
+ *     exec calls are re-entrant on distinct buffers (transform.py:46-52).
+ *   - exec calls are asynchronous and stream-ordered on `stream`
+ *     (a cudaStream_t, NULL = legacy default stream); they never allocate
+ *     and never synchronise.
+ */
+#ifndef SPLITFFT_B200_H
+#define SPLITFFT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFFT_ABI_VERSION 1
+
+/* status codes */
+#define SFFT_OK 0
+#define SFFT_EINVAL 1    /* bad argument            -> ValueError    */
+#define SFFT_ECAPACITY 2 /* size above a limit       -> CapacityError */
+#define SFFT_ECUDA 3     /* CUDA runtime failure     -> RuntimeError  */
+
+/* dtypes: the arithmetic type of the planes */
+#define SFFT_F32 0
+#define SFFT_F64 1
+
+/* algorithm, transform.py:41-43 (Algorithm.DIT / Algorithm.DIF) */
+#define SFFT_DIT 0
+#define SFFT_DIF 1
+
+/* direction: forward kernel exp(-j 2 pi n k / N), unnormalised; inverse by
+ * the channel-swap identity with 1/N (transform.py:273-298) */
+#define SFFT_FORWARD (-1)
+#define SFFT_INVERSE (+1)
+
+/* plan limit, transform.py:32 (MAX_PLAN_M) */
+#define SFFT_MAX_LOG2N 30
+
+typedef struct sfft_plan sfft_plan;
+
+/* ABI version of the loaded library (== SFFT_ABI_VERSION). */
+int sfft_abi_version(void);
+
+/* Thread-local message describing the last failed call on this thread. */
+const char *sfft_last_error(void);
+
+/* Replaces make_plan(m, algorithm, max_m=...) (transform.py:65-85).
+ * Validation order and messages follow the reference: log2n < 0 -> EINVAL
+ * "stage count m must be >= 0"; log2n > max_log2n -> ECAPACITY "exceeds the
+ * plan limit"; unknown algorithm -> EINVAL.  Builds the snapped stage-factor
+ * table on the host (twiddle.py:46-57, transform.py:82) and uploads it to
+ * `device`.  max_log2n <= SFFT_MAX_LOG2N. */
+int sfft_plan_create(int log2n, int dtype, int algorithm, int device,
+                     int max_log2n, sfft_plan **out);
+
+/* Same, with an explicit radix schedule: log2 of the register radix used by
+ * each fused pass (0 = library default).  Used by the tuner and tests. */
+int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device,
+                        int max_log2n, int log2_radix, sfft_plan **out);
+
+int sfft_plan_destroy(sfft_plan *plan);
+
+/* Plan introspection: log2n, dtype, algorithm, device, number of kernel
+ * launches per exec, register radix (log2).  Any pointer may be NULL. */
+int sfft_plan_info(const sfft_plan *plan, int *log2n, int *dtype,
+                   int *algorithm, int *device, int *launches_per_exec,
+                   int *log2_radix);
+
+/* Bytes of device workspace exec needs for `batch` rows (0 for the fused
+ * single-kernel path, log2n <= 12). */
+int sfft_workspace_bytes(const sfft_plan *plan, int64_t batch, size_t *bytes);
+
+/* The hot path.  Replaces the split->split composite
+ * SplitSignal(re, im) -> interleave -> fft|ifft -> deinterleave
+ * (service/app.py:43-52, transform.py:273-298), batched over `batch` rows.
+ * Planar SoA: x_re/x_im/y_re/y_im are device pointers to `batch` rows of
+ * 2^log2n elements of the plan dtype; row r of a plane starts at
+ * ptr + r*stride elements.  In place (y == x) is allowed.
+ * direction: SFFT_FORWARD or SFFT_INVERSE.  workspace: device pointer of at
+ * least sfft_workspace_bytes() bytes (may be NULL when that is 0). */
+int sfft_exec_split(const sfft_plan *plan, const void *x_re, const void *x_im,
+                    void *y_re, void *y_im, int64_t batch, int64_t in_stride,
+                    int64_t out_stride, int direction, void *workspace,
+                    void *stream);
+
+/* Same transform on the reference's interleaved layout
+ * (InterleavedBuffer, layout.py:46-86: [re0, im0, re1, im1, ...]).
+ * x/y point at `batch` rows of 2^log2n (re, im) pairs; strides count pairs.
+ * Replaces fft(plan, buf) / ifft(plan, buf) (transform.py:273-298). */
+int sfft_exec_interleaved(const sfft_plan *plan, const void *x, void *y,
+                          int64_t batch, int64_t in_stride, int64_t out_stride,
+                          int direction, void *workspace, void *stream);
+
+/* Host-only helpers (no GPU needed). */
+
+/* Stage-m factor table w[q] = cos - j sin of 2 pi q / 2^m, snapped, for
+ * q < 2^(log2n-1): wr = real, wi = imaginary part exactly as the reference's
+ * FftPlan.stage_factors[m-1] (transform.py:80-84).  Stage i uses
+ * w[q << (m-i)]. */
+int sfft_twiddle_table(int log2n, double *wr, double *wi);
+
+/* Census of count_flops (transform.py:312-335): out[0..4] = real_mults,
+ * real_adds, generic_rotations, quarter_turns, identity_rotations. */
+int sfft_count_flops(int log2n, int64_t *out5);
+
+/* Number of kernels this library has launched in this process. */
+int64_t sfft_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPLITFFT_B200_H */

@@ -1,0 +1,443 @@
+// sfft_abi.cu -- the C ABI declared in include/splitfft_b200.h.
+//
+// Plan construction mirrors make_plan (transform.py:65-85): same validation
+// order and messages, same snapped stage-factor values (twiddle.py:46-57,
+// transform.py:82) computed on the host with libm and uploaded once per
+// plan.  Exec is a pure stream-ordered launch sequence: one fused kernel for
+// log2n <= 12, otherwise one launch per stage group (sfft_pass.cuh).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/splitfft_b200.h"
+#include "sfft_fused.cuh"
+#include "sfft_launch.h"
+#include "sfft_pass.cuh"
+
+namespace sfft {
+static std::atomic<int64_t> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace sfft
+
+using namespace sfft;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what)
+{
+    return fail(SFFT_ECUDA, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+}
+
+// twiddle.py:46-57 then transform.py:82 (w = cos - 1j*sin as numpy forms it:
+// real part cos, imaginary part 0.0 - sin, so sin == 0 gives +0.0).
+inline void stage_factor(int i, int64_t q, double *wr, double *wi)
+{
+    double angle = 2.0 * M_PI * (double)q / (double)(int64_t(1) << i);
+    double c = cos(angle);
+    double s = sin(angle);
+    if (((4 * q) % (int64_t(1) << i)) == 0) {
+        c = nearbyint(c);
+        s = nearbyint(s);
+    }
+    c += 0.0;
+    s += 0.0;
+    *wr = c == 0.0 ? 0.0 : c;
+    *wi = 0.0 - s;
+}
+
+void stage_table(int i, int64_t count, double *wr, double *wi)
+{
+    // count <= 2^(i-1); parallel for the 2^27-entry tables of very long plans
+    const int64_t chunk = int64_t(1) << 20;
+    if (count <= chunk) {
+        for (int64_t q = 0; q < count; ++q) stage_factor(i, q, wr + q, wi + q);
+        return;
+    }
+    unsigned nt = std::thread::hardware_concurrency();
+    if (nt == 0) nt = 4;
+    if (nt > 32) nt = 32;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t) {
+        th.emplace_back([=] {
+            for (int64_t q0 = (int64_t)t * chunk; q0 < count; q0 += (int64_t)nt * chunk) {
+                int64_t q1 = q0 + chunk < count ? q0 + chunk : count;
+                for (int64_t q = q0; q < q1; ++q) stage_factor(i, q, wr + q, wi + q);
+            }
+        });
+    }
+    for (auto &x : th) x.join();
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev)
+    {
+        err = cudaGetDevice(&prev);
+        if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+struct Group {
+    int S, L;
+};
+
+}  // namespace
+
+struct sfft_plan {
+    int log2n = 0, dtype = 0, algo = 0, device = 0, lr = 0;
+    // fused path
+    void *d_tw = nullptr;          // vec2_t<T> table of stage tw_top
+    int tw_top = 0;
+    // large path
+    double2 *d_coarse = nullptr;
+    int coarse_log = 0;
+    double2 *d_fine = nullptr;
+    std::vector<Group> groups;
+};
+
+namespace {
+
+template <typename T>
+int upload_table(sfft_plan *p, int top)
+{
+    // stage `top` factors, 2^(top-1) entries, in the plan dtype
+    const int64_t h = top >= 1 ? int64_t(1) << (top - 1) : 1;
+    std::vector<double> wr((size_t)h, 1.0), wi((size_t)h, 0.0);
+    if (top >= 1) stage_table(top, h, wr.data(), wi.data());
+    std::vector<vec2_t<T>> host((size_t)h);
+    for (int64_t q = 0; q < h; ++q) {
+        host[q].x = (T)wr[q];
+        host[q].y = (T)wi[q];
+    }
+    cudaError_t e = cudaMalloc(&p->d_tw, sizeof(vec2_t<T>) * (size_t)h);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(twiddle table)");
+    e = cudaMemcpy(p->d_tw, host.data(), sizeof(vec2_t<T>) * (size_t)h, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(twiddle table)");
+    p->tw_top = top;
+    return SFFT_OK;
+}
+
+int upload_two_level(sfft_plan *p)
+{
+    // coarse: stage CL factors; fine: stage m factors for lo < 2^(m-CL)
+    const int m = p->log2n;
+    const int CL = m < 16 ? m : 16;
+    const int64_t hc = int64_t(1) << (CL - 1);
+    const int64_t hf = int64_t(1) << (m - CL);
+    std::vector<double> cr((size_t)hc), ci((size_t)hc), fr((size_t)hf), fi((size_t)hf);
+    stage_table(CL, hc, cr.data(), ci.data());
+    stage_table(m, hf, fr.data(), fi.data());
+    std::vector<double2> c2((size_t)hc), f2((size_t)hf);
+    for (int64_t q = 0; q < hc; ++q) c2[q] = make_double2(cr[q], ci[q]);
+    for (int64_t q = 0; q < hf; ++q) f2[q] = make_double2(fr[q], fi[q]);
+    cudaError_t e = cudaMalloc(&p->d_coarse, sizeof(double2) * (size_t)hc);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_fine, sizeof(double2) * (size_t)hf);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_coarse, c2.data(), sizeof(double2) * (size_t)hc, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_fine, f2.data(), sizeof(double2) * (size_t)hf, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "uploading two-level twiddles");
+    p->coarse_log = CL;
+    return SFFT_OK;
+}
+
+void free_plan(sfft_plan *p)
+{
+    if (!p) return;
+    if (p->d_tw) cudaFree(p->d_tw);
+    if (p->d_coarse) cudaFree(p->d_coarse);
+    if (p->d_fine) cudaFree(p->d_fine);
+    delete p;
+}
+
+std::vector<Group> split_groups(int m)
+{
+    const int G = (m + kPassMaxL - 1) / kPassMaxL;
+    std::vector<Group> g;
+    int S = 0;
+    for (int k = 0; k < G; ++k) {
+        int L = m / G + (k < m % G ? 1 : 0);
+        g.push_back({S, L});
+        S += L;
+    }
+    return g;
+}
+
+int validate_exec(const sfft_plan *p, int64_t batch, int64_t is, int64_t os, int direction)
+{
+    if (!p) return fail(SFFT_EINVAL, "plan is NULL");
+    if (batch < 0) return fail(SFFT_EINVAL, "batch must be >= 0, got %lld", (long long)batch);
+    const int64_t n = int64_t(1) << p->log2n;
+    if (batch > 1 && (is < n || os < n))
+        return fail(SFFT_EINVAL, "row strides (%lld, %lld) must be >= N = %lld", (long long)is,
+                    (long long)os, (long long)n);
+    if (direction != SFFT_FORWARD && direction != SFFT_INVERSE)
+        return fail(SFFT_EINVAL, "direction must be -1 (forward) or +1 (inverse), got %d", direction);
+    if (batch > (int64_t(1) << 40)) return fail(SFFT_ECAPACITY, "batch %lld exceeds the launch limit", (long long)batch);
+    return SFFT_OK;
+}
+
+int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, void *y1, bool il,
+                int64_t batch, int64_t is, int64_t os, int direction, void *workspace, void *stream)
+{
+    int rc = validate_exec(p, batch, is, os, direction);
+    if (rc) return rc;
+    if (batch == 0) return SFFT_OK;
+    if (!x0 || !y0 || (!il && (!x1 || !y1))) return fail(SFFT_EINVAL, "NULL signal pointer");
+    DeviceGuard dg(p->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool inv = direction == SFFT_INVERSE;
+    const int m = p->log2n;
+    const double scale = inv ? 1.0 / (double)(int64_t(1) << m) : 1.0;
+
+    if (m <= kFusedMaxLog) {
+        FusedLaunchFn fn = fused_launcher_algo(p->dtype, m, p->lr, p->algo == SFFT_DIF, il);
+        if (!fn) return fail(SFFT_EINVAL, "no fused kernel for log2n=%d radix=2^%d layout=%s", m, p->lr,
+                             il ? "interleaved" : "planar");
+        FusedArgs a;
+        a.x0 = x0;
+        a.x1 = x1;
+        a.y0 = y0;
+        a.y1 = y1;
+        a.tw = p->d_tw;
+        a.batch = batch;
+        a.in_stride = is;
+        a.out_stride = os;
+        a.inverse = inv ? 1 : 0;
+        a.scale = scale;
+        cudaError_t e = fn(a, p->algo == SFFT_DIF, il, st);
+        if (e != cudaSuccess) return cuda_fail(e, "fused kernel launch");
+        return SFFT_OK;
+    }
+
+    // multi-launch schedule: groups in order (DIT) or reverse order (DIF)
+    if (!workspace) return fail(SFFT_EINVAL, "log2n=%d needs a workspace (sfft_workspace_bytes)", m);
+    const int64_t n = int64_t(1) << m;
+    const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
+    const int G = (int)p->groups.size();
+    char *ws = (char *)workspace;
+    const size_t plane = (size_t)batch * (size_t)n * esz;
+    void *bufA[2] = {ws, ws + plane};
+    void *bufB[2] = {ws + 2 * plane, ws + 3 * plane};
+    const int TJ = pass_tile(p->dtype);
+    for (int k = 0; k < G; ++k) {
+        const Group gr = p->algo == SFFT_DIF ? p->groups[G - 1 - k] : p->groups[k];
+        PassLaunchFn fn = pass_launcher(p->dtype, gr.L);
+        if (!fn) return fail(SFFT_EINVAL, "no pass kernel for L=%d", gr.L);
+        PassArgs a;
+        memset(&a, 0, sizeof a);
+        const bool first = k == 0, last = k == G - 1;
+        void **src = (k % 2 == 1) ? bufA : bufB;   // k-1 wrote A when k-1 even
+        void **dst = last ? nullptr : ((k % 2 == 0) ? bufA : bufB);
+        if (first) {
+            a.x0 = x0;
+            a.x1 = x1;
+            a.in_stride = is;
+        } else {
+            a.x0 = src[0];
+            a.x1 = src[1];
+            a.in_stride = n;
+        }
+        if (last) {
+            a.y0 = y0;
+            a.y1 = y1;
+            a.out_stride = os;
+        } else {
+            a.y0 = dst[0];
+            a.y1 = dst[1];
+            a.out_stride = n;
+        }
+        a.batch = batch;
+        a.m = m;
+        a.S = gr.S;
+        a.swap_in = first && inv;
+        a.swap_out = last && inv;
+        a.scale = last ? scale : 1.0;
+        a.tw = p->d_tw;
+        a.tw_top = p->tw_top;
+        a.coarse = p->d_coarse;
+        a.coarse_log = p->coarse_log;
+        a.fine = p->d_fine;
+        const int64_t grid = batch * ((n >> gr.L) / TJ);
+        cudaError_t e = fn(a, p->algo == SFFT_DIF, first && il, last && il, grid, st);
+        if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");
+    }
+    return SFFT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sfft_abi_version(void) { return SFFT_ABI_VERSION; }
+
+const char *sfft_last_error(void) { return g_err.c_str(); }
+
+int64_t sfft_launch_count(void) { return g_launches.load(); }
+
+int sfft_twiddle_table(int log2n, double *wr, double *wi)
+{
+    if (log2n < 1 || log2n > SFFT_MAX_LOG2N) return fail(SFFT_EINVAL, "log2n must be in [1, %d], got %d", SFFT_MAX_LOG2N, log2n);
+    if (!wr || !wi) return fail(SFFT_EINVAL, "NULL output pointer");
+    stage_table(log2n, int64_t(1) << (log2n - 1), wr, wi);
+    return SFFT_OK;
+}
+
+int sfft_count_flops(int log2n, int64_t *out5)
+{
+    // transform.py:312-335 with the closed forms pinned by
+    // test_transform.py:323-332: identity = m, quarter = m-1, generic = N-2m
+    if (log2n < 0) return fail(SFFT_EINVAL, "stage count m must be >= 0, got %d", log2n);
+    if (log2n > SFFT_MAX_LOG2N) return fail(SFFT_ECAPACITY, "m=%d exceeds the plan limit max_m=%d", log2n, SFFT_MAX_LOG2N);
+    if (!out5) return fail(SFFT_EINVAL, "NULL output pointer");
+    const int64_t m = log2n, n = int64_t(1) << log2n;
+    const int64_t ident = m, quarter = m > 0 ? m - 1 : 0, generic = m > 0 ? n - 2 * m : 0;
+    out5[0] = 4 * generic;
+    out5[1] = 4 * (n >> 1) * m;
+    out5[2] = generic;
+    out5[3] = quarter;
+    out5[4] = ident;
+    return SFFT_OK;
+}
+
+int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max_log2n, int log2_radix,
+                        sfft_plan **out)
+{
+    if (!out) return fail(SFFT_EINVAL, "out is NULL");
+    *out = nullptr;
+    // validation order of make_plan (transform.py:72-76)
+    if (log2n < 0) return fail(SFFT_EINVAL, "stage count m must be >= 0, got %d", log2n);
+    if (log2n > max_log2n) return fail(SFFT_ECAPACITY, "m=%d exceeds the plan limit max_m=%d", log2n, max_log2n);
+    if (log2n > SFFT_MAX_LOG2N)
+        return fail(SFFT_ECAPACITY, "m=%d exceeds the plan limit max_m=%d", log2n, SFFT_MAX_LOG2N);
+    if (algorithm != SFFT_DIT && algorithm != SFFT_DIF)
+        return fail(SFFT_EINVAL, "%d is not a valid Algorithm (0 = dit, 1 = dif)", algorithm);
+    if (dtype != SFFT_F32 && dtype != SFFT_F64) return fail(SFFT_EINVAL, "unknown dtype %d", dtype);
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
+    if (device < 0 || device >= ndev) return fail(SFFT_EINVAL, "device %d out of range (%d devices)", device, ndev);
+
+    sfft_plan *p = new sfft_plan;
+    p->log2n = log2n;
+    p->dtype = dtype;
+    p->algo = algorithm;
+    p->device = device;
+    DeviceGuard dg(device);
+    if (dg.err != cudaSuccess) {
+        delete p;
+        return cuda_fail(dg.err, "cudaSetDevice");
+    }
+    int rc = SFFT_OK;
+    if (log2n <= kFusedMaxLog) {
+        int lr = log2_radix > 0 ? log2_radix : fused_default_lr(dtype, log2n);
+        if (log2n == 0) lr = 0;
+        if (lr > log2n) lr = log2n;
+        if (!fused_launcher_algo(dtype, log2n, lr, algorithm == SFFT_DIF, false)) {
+            delete p;
+            return fail(SFFT_EINVAL, "radix 2^%d is not available for log2n=%d", lr, log2n);
+        }
+        p->lr = lr;
+        rc = dtype == SFFT_F32 ? upload_table<float>(p, log2n) : upload_table<double>(p, log2n);
+    } else {
+        p->lr = pass_default_lr(dtype);
+        p->groups = split_groups(log2n);
+        if (dtype == SFFT_F32) {
+            rc = upload_table<float>(p, kFusedMaxLog);
+            if (rc == SFFT_OK) rc = upload_two_level(p);
+        } else {
+            rc = upload_table<double>(p, log2n);
+        }
+    }
+    if (rc != SFFT_OK) {
+        free_plan(p);
+        return rc;
+    }
+    *out = p;
+    return SFFT_OK;
+}
+
+int sfft_plan_create(int log2n, int dtype, int algorithm, int device, int max_log2n, sfft_plan **out)
+{
+    return sfft_plan_create_ex(log2n, dtype, algorithm, device, max_log2n, 0, out);
+}
+
+int sfft_plan_destroy(sfft_plan *plan)
+{
+    if (!plan) return SFFT_OK;
+    DeviceGuard dg(plan->device);
+    free_plan(plan);
+    return SFFT_OK;
+}
+
+int sfft_plan_info(const sfft_plan *p, int *log2n, int *dtype, int *algorithm, int *device, int *launches,
+                   int *log2_radix)
+{
+    if (!p) return fail(SFFT_EINVAL, "plan is NULL");
+    if (log2n) *log2n = p->log2n;
+    if (dtype) *dtype = p->dtype;
+    if (algorithm) *algorithm = p->algo;
+    if (device) *device = p->device;
+    if (launches) *launches = p->log2n <= kFusedMaxLog ? 1 : (int)p->groups.size();
+    if (log2_radix) *log2_radix = p->lr;
+    return SFFT_OK;
+}
+
+int sfft_workspace_bytes(const sfft_plan *p, int64_t batch, size_t *bytes)
+{
+    if (!p) return fail(SFFT_EINVAL, "plan is NULL");
+    if (!bytes) return fail(SFFT_EINVAL, "bytes is NULL");
+    if (batch < 0) return fail(SFFT_EINVAL, "batch must be >= 0, got %lld", (long long)batch);
+    if (p->log2n <= kFusedMaxLog) {
+        *bytes = 0;
+        return SFFT_OK;
+    }
+    const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
+    const size_t planes = p->groups.size() >= 3 ? 4 : 2;   // ping-pong A (and B)
+    *bytes = planes * (size_t)batch * ((size_t)1 << p->log2n) * esz;
+    return SFFT_OK;
+}
+
+int sfft_exec_split(const sfft_plan *plan, const void *x_re, const void *x_im, void *y_re, void *y_im,
+                    int64_t batch, int64_t in_stride, int64_t out_stride, int direction, void *workspace,
+                    void *stream)
+{
+    return exec_common(plan, x_re, x_im, y_re, y_im, false, batch, in_stride, out_stride, direction, workspace,
+                       stream);
+}
+
+int sfft_exec_interleaved(const sfft_plan *plan, const void *x, void *y, int64_t batch, int64_t in_stride,
+                          int64_t out_stride, int direction, void *workspace, void *stream)
+{
+    return exec_common(plan, x, nullptr, y, nullptr, true, batch, in_stride, out_stride, direction, workspace,
+                       stream);
+}
+
+}  // extern "C"

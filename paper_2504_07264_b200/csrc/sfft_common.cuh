@@ -1,0 +1,176 @@
+// sfft_common.cuh -- shared device helpers for the split-format DFT kernels.
+//
+// Arithmetic contract: every kernel executes the
+// reference's radix-2 stage factorization literally (PAPER.md:149-165,
+// transform.py:131-150): DIT stage i does  t = b*w; b = a - t; a = a + t,
+// DIF stage i does  t = a - b; a = a + b; b = t*w, with w the stage-i factor
+// cos - j sin from the snapped table (twiddle.py:46-57).  Stage 1 never
+// multiplies (transform.py:123-128).  The complex product is rounded the way
+// numpy rounds complex128 multiply on x86-64 (re = fma(ar,br,-(ai*bi)),
+// im = fma(ar,bi,ai*br)), with explicit _rn intrinsics so nvcc cannot
+// re-contract it.  In fp64 this makes the GPU output bit-identical to the
+// reference; in fp32 it is the same op sequence in single precision.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sfft {
+
+template <typename T> struct Vec2;
+template <> struct Vec2<float> { using type = float2; };
+template <> struct Vec2<double> { using type = double2; };
+template <typename T> using vec2_t = typename Vec2<T>::type;
+
+__host__ __device__ constexpr int brev(int f, int bits)
+{
+    int r = 0;
+    for (int b = 0; b < bits; ++b) { r = (r << 1) | (f & 1); f >>= 1; }
+    return r;
+}
+
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+
+__device__ __forceinline__ void cmul(float ar, float ai, float br, float bi, float &cr, float &ci)
+{
+    cr = __fmaf_rn(ar, br, -__fmul_rn(ai, bi));
+    ci = __fmaf_rn(ar, bi, __fmul_rn(ai, br));
+}
+
+__device__ __forceinline__ void cmul(double ar, double ai, double br, double bi, double &cr, double &ci)
+{
+    cr = __fma_rn(ar, br, -__dmul_rn(ai, bi));
+    ci = __fma_rn(ar, bi, __dmul_rn(ai, br));
+}
+
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// Read-only twiddle fetch (L1-resident table; never written by a kernel).
+__device__ __forceinline__ float2 ldtw(const float2 *p) { return __ldg(p); }
+__device__ __forceinline__ double2 ldtw(const double2 *p) { return __ldg(p); }
+
+// Streaming (evict-first) global accesses for the signal planes: every
+// element is read once and written once per launch.
+__device__ __forceinline__ float ld_stream(const float *p) { return __ldcs(p); }
+__device__ __forceinline__ double ld_stream(const double *p) { return __ldcs(p); }
+__device__ __forceinline__ float2 ld_stream(const float2 *p) { return __ldcs(p); }
+__device__ __forceinline__ double2 ld_stream(const double2 *p) { return __ldcs(p); }
+__device__ __forceinline__ void st_stream(float *p, float v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double *p, double v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(float2 *p, float2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }
+
+// Twiddle source for the stages of one launch.
+//   Direct: stage i, index q -> tab[q << (top - i)] where tab is the
+//           stage-`top` factor table (every stage table is a bitwise strided
+//           view of it).
+//   TwoLevel (fp32, stages above the coarse table, large N only): the
+//           factor is coarse[hi] * fine[lo] evaluated in fp64 and rounded.
+template <typename T>
+struct TwDirect {
+    const vec2_t<T> *tab;
+    int top;
+    __device__ __forceinline__ vec2_t<T> get(int i, int64_t q) const
+    {
+        return ldtw(tab + (q << (top - i)));
+    }
+};
+
+template <typename T>
+struct TwTwoLevel {
+    const vec2_t<T> *tab;      // direct table of stage `top` (top <= coarse_log)
+    int top;
+    const double2 *coarse;     // stage coarse_log factors, 2^(coarse_log-1) entries
+    int coarse_log;
+    const double2 *fine;       // exp(-j 2 pi lo / 2^m), lo < 2^(m - coarse_log)
+    int m;
+    __device__ __forceinline__ vec2_t<T> get(int i, int64_t q) const
+    {
+        if (i <= top) return ldtw(tab + (q << (top - i)));
+        const int64_t qq = q << (m - i);
+        const int fb = m - coarse_log;
+        const double2 a = __ldg(coarse + (qq >> fb));
+        const double2 b = __ldg(fine + (qq & ((int64_t(1) << fb) - 1)));
+        double r, im;
+        cmul(a.x, a.y, b.x, b.y, r, im);
+        vec2_t<T> w;
+        w.x = (T)r;
+        w.y = (T)im;
+        return w;
+    }
+};
+
+// K consecutive DIT stages (global stages gs+1 .. gs+K) on the 2^K values
+// v[0..2^K) of one virtual thread.  Register position p holds, before stage
+// t, the (size 2^(gs+t-1)) partial transform of sub-sequence (p mod
+// 2^K/2^(t-1)) at frequency index rev_{t-1}(p / (2^K/2^(t-1))); the
+// stage-(gs+t) factor index is q = cbase + (f << gs).  After the K stages
+// register rev_K(f) holds output frequency f.  Validated bitwise against the
+// reference by tests/test_schedule_model.py (a numpy restatement of exactly
+// this index map).
+template <typename T, int K, typename TW>
+__device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, int64_t cbase, const TW &tw)
+{
+#pragma unroll
+    for (int t = 1; t <= K; ++t) {
+        const int half = (1 << K) >> t;
+        const int i = gs + t;
+#pragma unroll
+        for (int f = 0; f < (1 << (t - 1)); ++f) {
+            const int rf = brev(f, t - 1) * 2 * half;
+            vec2_t<T> w;
+            if (i > 1) w = tw.get(i, cbase + ((int64_t)f << gs));
+#pragma unroll
+            for (int r = 0; r < half; ++r) {
+                const int p1 = r + rf, p2 = p1 + half;
+                T tr, ti;
+                if (i > 1) {
+                    cmul(vr[p2], vi[p2], w.x, w.y, tr, ti);
+                } else {
+                    tr = vr[p2];
+                    ti = vi[p2];
+                }
+                vr[p2] = sub_rn(vr[p1], tr);
+                vi[p2] = sub_rn(vi[p1], ti);
+                vr[p1] = add_rn(vr[p1], tr);
+                vi[p1] = add_rn(vi[p1], ti);
+            }
+        }
+    }
+}
+
+// Transpose of dit_stages: DIF stages gs+K .. gs+1 (descending), same
+// register map run backwards.
+template <typename T, int K, typename TW>
+__device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, int64_t cbase, const TW &tw)
+{
+#pragma unroll
+    for (int t = K; t >= 1; --t) {
+        const int half = (1 << K) >> t;
+        const int i = gs + t;
+#pragma unroll
+        for (int f = 0; f < (1 << (t - 1)); ++f) {
+            const int rf = brev(f, t - 1) * 2 * half;
+            vec2_t<T> w;
+            if (i > 1) w = tw.get(i, cbase + ((int64_t)f << gs));
+#pragma unroll
+            for (int r = 0; r < half; ++r) {
+                const int p1 = r + rf, p2 = p1 + half;
+                const T tr = sub_rn(vr[p1], vr[p2]);
+                const T ti = sub_rn(vi[p1], vi[p2]);
+                vr[p1] = add_rn(vr[p1], vr[p2]);
+                vi[p1] = add_rn(vi[p1], vi[p2]);
+                if (i > 1) {
+                    cmul(tr, ti, w.x, w.y, vr[p2], vi[p2]);
+                } else {
+                    vr[p2] = tr;
+                    vi[p2] = ti;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace sfft

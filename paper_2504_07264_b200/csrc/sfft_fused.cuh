@@ -1,0 +1,298 @@
+// sfft_fused.cuh -- one fused kernel per batch tile for N = 2^LOGN <= 4096.
+//
+// Replaces transform.py:208-270 (fft_dit / fft_dif) batched over rows.
+// Each signal is split over P = N / R threads that each hold R = 2^LR complex
+// values in registers.  The m radix-2 stages are executed LR at a time
+// ("passes"); pass p runs stages p*LR+1 .. p*LR+K_p of the reference's
+// factorization in registers (sfft_common.cuh dit_stages/dif_stages) and
+// exchanges data between passes through shared memory in Stockham order, so
+// the bit-reversal permutation S of the paper costs no pass of its own:
+//   DIT pass p (ns = 2^(p*LR), R' = 2^K_p), virtual thread j:
+//     reads  in [ j + r * N/R' ]                 r < R'
+//     writes out[ (j>>s)*ns*R' + (j&(ns-1)) + ns*f ] = reg[rev(f)]
+//   DIF runs the passes in reverse with reads and writes exchanged.
+// The first pass reads global memory directly and the last pass writes it
+// directly; both patterns are unit-stride across the threads of a signal, so
+// every warp-wide access covers whole 32-byte sectors.  Shared-memory
+// addresses are padded by one element per R (phys = e + e/R) which makes
+// both exchange patterns bank-conflict free for the shipped radix choices.
+#pragma once
+#include "sfft_common.cuh"
+
+namespace sfft {
+
+struct FusedArgs {
+    const void *x0, *x1;   // planar: re, im planes; interleaved: x0 = pairs
+    void *y0, *y1;
+    const void *tw;        // vec2_t<T>[N/2] stage-LOGN factor table
+    int64_t batch;
+    int64_t in_stride, out_stride;   // elements (planar) or pairs (interleaved)
+    int inverse;           // channel-swap inverse (transform.py:286-298)
+    double scale;          // 1/N for the inverse, 1 otherwise
+};
+
+// Global-memory view of the caller's rows.
+template <typename T, bool IL>
+struct GIO;
+
+template <typename T>
+struct GIO<T, false> {
+    const T *xr, *xi;
+    T *yr, *yi;
+    int64_t is, os;
+    bool inv;
+    T scale;
+    __device__ __forceinline__ GIO(const FusedArgs &a)
+        : xr((const T *)a.x0), xi((const T *)a.x1), yr((T *)a.y0), yi((T *)a.y1),
+          is(a.in_stride), os(a.out_stride), inv(a.inverse != 0), scale((T)a.scale) {}
+    __device__ __forceinline__ void load(int64_t row, int64_t e, T &re, T &im) const
+    {
+        const T a = ld_stream(xr + row * is + e);
+        const T b = ld_stream(xi + row * is + e);
+        re = inv ? b : a;
+        im = inv ? a : b;
+    }
+    __device__ __forceinline__ void store(int64_t row, int64_t e, T re, T im) const
+    {
+        if (inv) {
+            st_stream(yr + row * os + e, im * scale);
+            st_stream(yi + row * os + e, re * scale);
+        } else {
+            st_stream(yr + row * os + e, re);
+            st_stream(yi + row * os + e, im);
+        }
+    }
+};
+
+template <typename T>
+struct GIO<T, true> {
+    using V = vec2_t<T>;
+    const V *x;
+    V *y;
+    int64_t is, os;
+    bool inv;
+    T scale;
+    __device__ __forceinline__ GIO(const FusedArgs &a)
+        : x((const V *)a.x0), y((V *)a.y0), is(a.in_stride), os(a.out_stride),
+          inv(a.inverse != 0), scale((T)a.scale) {}
+    __device__ __forceinline__ void load(int64_t row, int64_t e, T &re, T &im) const
+    {
+        const V v = ld_stream(x + row * is + e);
+        re = inv ? v.y : v.x;
+        im = inv ? v.x : v.y;
+    }
+    __device__ __forceinline__ void store(int64_t row, int64_t e, T re, T im) const
+    {
+        V v;
+        if (inv) {
+            v.x = im * scale;
+            v.y = re * scale;
+        } else {
+            v.x = re;
+            v.y = im;
+        }
+        st_stream(y + row * os + e, v);
+    }
+};
+
+template <int LOGN, int LR_REQ>
+struct FusedShape {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int LR = LOGN == 0 ? 0 : cmin(LR_REQ, LOGN);
+    static constexpr int R = 1 << LR;
+    static constexpr int P = N / R;                       // threads per signal
+    static constexpr int NT = P > 256 ? P : 256;          // threads per block
+    static constexpr int S = NT / P;                      // signals per block
+    static constexpr int NPASS = LOGN == 0 ? 0 : (LOGN + LR - 1) / LR;
+    static constexpr int SSTR = N + (N >> LR);            // padded plane stride
+    template <typename T>
+    static constexpr int smem_bytes() { return NPASS >= 2 ? 2 * S * SSTR * (int)sizeof(T) : 0; }
+};
+
+template <int LR>
+__device__ __forceinline__ int sphys(int e) { return e + (e >> LR); }
+
+template <int P>
+__device__ __forceinline__ void sig_sync()
+{
+    if constexpr (P <= 32) __syncwarp(); else __syncthreads();
+}
+
+// ---- DIT pass p -----------------------------------------------------------
+template <typename T, int LOGN, int LR_REQ, bool IL, int p>
+__device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool valid,
+                                         T *sr, T *si, const GIO<T, IL> &io,
+                                         const TwDirect<T> &tw)
+{
+    using Sh = FusedShape<LOGN, LR_REQ>;
+    constexpr int N = Sh::N, R = Sh::R, P = Sh::P, LR = Sh::LR;
+    constexpr int SP = p * LR;
+    constexpr int KP = cmin(LR, LOGN - SP);
+    constexpr int RP = 1 << KP, U = R / RP, NS = 1 << SP;
+    constexpr bool FIRST = p == 0, LAST = p == Sh::NPASS - 1;
+
+    // gather this pass's inputs
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int j = t + P * u;
+#pragma unroll
+        for (int r = 0; r < RP; ++r) {
+            const int e = j + r * (N / RP);
+            if constexpr (FIRST) {
+                if (valid) io.load(row, e, vr[u * RP + r], vi[u * RP + r]);
+                else { vr[u * RP + r] = T(0); vi[u * RP + r] = T(0); }
+            } else {
+                vr[u * RP + r] = sr[sphys<LR>(e)];
+                vi[u * RP + r] = si[sphys<LR>(e)];
+            }
+        }
+    }
+    // stages SP+1 .. SP+KP
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int j = t + P * u;
+        dit_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (int64_t)(j & (NS - 1)), tw);
+    }
+    // scatter in Stockham order
+    if constexpr (!LAST) {
+        if constexpr (!FIRST) sig_sync<P>();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = t + P * u;
+            const int base = (j >> SP) * NS * RP + (j & (NS - 1));
+#pragma unroll
+            for (int f = 0; f < RP; ++f) {
+                const int e = base + NS * f;
+                sr[sphys<LR>(e)] = vr[u * RP + brev(f, KP)];
+                si[sphys<LR>(e)] = vi[u * RP + brev(f, KP)];
+            }
+        }
+        sig_sync<P>();
+    } else {
+        if (valid) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = t + P * u;     // NS*RP == N here, so (j >> SP) == 0
+#pragma unroll
+                for (int f = 0; f < RP; ++f)
+                    io.store(row, j + NS * f, vr[u * RP + brev(f, KP)], vi[u * RP + brev(f, KP)]);
+            }
+        }
+    }
+}
+
+template <typename T, int LOGN, int LR_REQ, bool IL, int p>
+__device__ __forceinline__ void dit_from(T *vr, T *vi, int t, int64_t row, bool valid,
+                                         T *sr, T *si, const GIO<T, IL> &io, const TwDirect<T> &tw)
+{
+    if constexpr (p < FusedShape<LOGN, LR_REQ>::NPASS) {
+        dit_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw);
+        dit_from<T, LOGN, LR_REQ, IL, p + 1>(vr, vi, t, row, valid, sr, si, io, tw);
+    }
+}
+
+// ---- DIF pass p (executed for p = NPASS-1 .. 0) --------------------------
+template <typename T, int LOGN, int LR_REQ, bool IL, int p>
+__device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool valid,
+                                         T *sr, T *si, const GIO<T, IL> &io,
+                                         const TwDirect<T> &tw)
+{
+    using Sh = FusedShape<LOGN, LR_REQ>;
+    constexpr int N = Sh::N, R = Sh::R, P = Sh::P, LR = Sh::LR;
+    constexpr int SP = p * LR;
+    constexpr int KP = cmin(LR, LOGN - SP);
+    constexpr int RP = 1 << KP, U = R / RP, NS = 1 << SP;
+    constexpr bool FIRST = p == Sh::NPASS - 1, LAST = p == 0;
+
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int j = t + P * u;
+        const int base = (j >> SP) * NS * RP + (j & (NS - 1));
+#pragma unroll
+        for (int f = 0; f < RP; ++f) {
+            const int e = base + NS * f;
+            const int d = u * RP + brev(f, KP);
+            if constexpr (FIRST) {
+                if (valid) io.load(row, e, vr[d], vi[d]);
+                else { vr[d] = T(0); vi[d] = T(0); }
+            } else {
+                vr[d] = sr[sphys<LR>(e)];
+                vi[d] = si[sphys<LR>(e)];
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int j = t + P * u;
+        dif_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (int64_t)(j & (NS - 1)), tw);
+    }
+    if constexpr (!LAST) {
+        if constexpr (!FIRST) sig_sync<P>();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = t + P * u;
+#pragma unroll
+            for (int r = 0; r < RP; ++r) {
+                const int e = j + r * (N / RP);
+                sr[sphys<LR>(e)] = vr[u * RP + r];
+                si[sphys<LR>(e)] = vi[u * RP + r];
+            }
+        }
+        sig_sync<P>();
+    } else {
+        if (valid) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = t + P * u;
+#pragma unroll
+                for (int r = 0; r < RP; ++r)
+                    io.store(row, j + r * (N / RP), vr[u * RP + r], vi[u * RP + r]);
+            }
+        }
+    }
+}
+
+template <typename T, int LOGN, int LR_REQ, bool IL, int p>
+__device__ __forceinline__ void dif_from(T *vr, T *vi, int t, int64_t row, bool valid,
+                                         T *sr, T *si, const GIO<T, IL> &io, const TwDirect<T> &tw)
+{
+    if constexpr (p >= 0) {
+        dif_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw);
+        dif_from<T, LOGN, LR_REQ, IL, p - 1>(vr, vi, t, row, valid, sr, si, io, tw);
+    }
+}
+
+template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL>
+__global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT)
+sfft_fused_kernel(const FusedArgs a)
+{
+    using Sh = FusedShape<LOGN, LR_REQ>;
+    constexpr int R = Sh::R, P = Sh::P, S = Sh::S, SSTR = Sh::SSTR;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T *sbase = reinterpret_cast<T *>(smem_raw);
+
+    const int tid = threadIdx.x;
+    const int sl = tid / P, t = tid % P;
+    const int64_t row = (int64_t)blockIdx.x * S + sl;
+    const bool valid = row < a.batch;
+    const GIO<T, IL> io(a);
+    const TwDirect<T> tw{reinterpret_cast<const vec2_t<T> *>(a.tw), LOGN};
+
+    if constexpr (LOGN == 0) {
+        if (valid) {
+            T re, im;
+            io.load(row, 0, re, im);
+            io.store(row, 0, re, im);
+        }
+    } else {
+        T vr[R], vi[R];
+        T *sr = sbase + sl * SSTR;
+        T *si = sbase + S * SSTR + sl * SSTR;
+        if constexpr (DIF)
+            dif_from<T, LOGN, LR_REQ, IL, Sh::NPASS - 1>(vr, vi, t, row, valid, sr, si, io, tw);
+        else
+            dit_from<T, LOGN, LR_REQ, IL, 0>(vr, vi, t, row, valid, sr, si, io, tw);
+    }
+}
+
+}  // namespace sfft

@@ -1,0 +1,36 @@
+// sfft_launch.h -- host-side launcher registry shared by the generated
+// instantiation units (sfft_inst_*.cu) and the C ABI (sfft_abi.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sfft {
+
+struct FusedArgs;
+struct PassArgs;
+
+// Launch one fused kernel (N = 2^logn <= 4096) over a.batch rows.
+using FusedLaunchFn = cudaError_t (*)(const FusedArgs &a, bool dif, bool interleaved, cudaStream_t st);
+// Launch one pass group (2^L-point sub-problems) over a.batch rows.
+using PassLaunchFn = cudaError_t (*)(const PassArgs &a, bool dif, bool il_in, bool il_out,
+                                     int64_t grid, cudaStream_t st);
+
+constexpr int kFusedMaxLog = 12;
+constexpr int kMaxRadixLog = 5;
+constexpr int kPassMinL = 5, kPassMaxL = 8;
+
+// Registry lookups (nullptr when the combination was not instantiated).
+// dtype: 0 = f32, 1 = f64.  Interleaved variants exist only for the
+// default radix of each size.  The returned fused launcher is bound to
+// (dif, il) already and ignores those two arguments.
+FusedLaunchFn fused_launcher_algo(int dtype, int logn, int lr, bool dif, bool il);
+int fused_default_lr(int dtype, int logn);
+PassLaunchFn pass_launcher(int dtype, int L);
+int pass_tile(int dtype);           // TJ: sub-problems per CTA
+int pass_default_lr(int dtype);
+PassLaunchFn pass_launcher_f32(int L);
+PassLaunchFn pass_launcher_f64(int L);
+
+void count_launch();
+
+}  // namespace sfft

@@ -1,0 +1,348 @@
+"""Plans and transforms on the GPU (mirrors splitfft/transform.py).
+
+Public surface kept from the reference: ``MAX_PLAN_M``, ``Algorithm``,
+``FftPlan``, ``make_plan``, ``fft``, ``fft_dit``, ``fft_dif``, ``ifft``,
+``FlopReport``, ``count_flops`` (transform.py:32-335), plus the batched
+split->split drop-in ``fft_split`` / ``ifft_split`` -- the planar
+``(x_re, x_im) -> (y_re, y_im)`` form of the reference's service path
+(service/app.py:43-52).
+
+Every transform runs on the GPU through the C ABI (``_ffi``); there is no
+CPU fallback.  Host inputs (numpy arrays, CPU tensors) are copied to the
+current CUDA device, transformed there and copied back, so reference users
+can switch without touching their arrays; with no CUDA device the call
+raises.
+"""
+
+import enum
+import ctypes
+import threading
+from dataclasses import dataclass
+from functools import lru_cache
+
+import numpy as np
+import torch
+
+from . import _ffi
+from .errors import CapacityError
+from .layout import InterleavedBuffer, SplitSignal, bit_reverse_indices, is_power_of_two
+from .twiddle import TwiddleTable, build_twiddle_table, stage_factor_table
+
+MAX_PLAN_M = _ffi.SFFT_MAX_LOG2N   # transform.py:32
+
+_DTYPE_CODE = {torch.float32: _ffi.SFFT_F32, torch.float64: _ffi.SFFT_F64}
+
+
+class Algorithm(enum.Enum):
+    DIT = "dit"
+    DIF = "dif"
+
+
+def _resolve_device(device) -> torch.device:
+    if device is None:
+        if not torch.cuda.is_available():
+            raise RuntimeError("splitfft-b200 needs a CUDA device (there is no CPU fallback)")
+        return torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise ValueError(f"plans live on a CUDA device, got {device} (there is no CPU fallback)")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return device
+
+
+class FftPlan:
+    """Device-resident tables for transforms of one size (transform.py:46-62).
+
+    Immutable and safe to share across threads; every call works on its own
+    buffers (and its own workspace for log2 N > 12).
+    """
+
+    __slots__ = ("m", "algorithm", "dtype", "device", "_handle", "_lock", "_tables", "__weakref__")
+
+    def __init__(self, m, algorithm, dtype, device, handle):
+        object.__setattr__(self, "m", m)
+        object.__setattr__(self, "algorithm", algorithm)
+        object.__setattr__(self, "dtype", dtype)
+        object.__setattr__(self, "device", device)
+        object.__setattr__(self, "_handle", handle)
+        object.__setattr__(self, "_lock", threading.Lock())
+        object.__setattr__(self, "_tables", None)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("FftPlan is immutable")
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h:
+            try:
+                _ffi.lib.sfft_plan_destroy(h)
+            except Exception:
+                pass
+
+    def __repr__(self):
+        return (f"FftPlan(m={self.m}, algorithm={self.algorithm}, dtype={self.dtype}, "
+                f"device={self.device}, radix=2^{self.radix_log}, launches={self.launches_per_exec})")
+
+    @property
+    def sample_count(self) -> int:
+        return 1 << self.m
+
+    def _info(self):
+        vals = [ctypes.c_int() for _ in range(6)]
+        _ffi.check(_ffi.lib.sfft_plan_info(self._handle, *[ctypes.byref(v) for v in vals]))
+        return [v.value for v in vals]
+
+    @property
+    def launches_per_exec(self) -> int:
+        return self._info()[4]
+
+    @property
+    def radix_log(self) -> int:
+        return self._info()[5]
+
+    def workspace_bytes(self, batch: int) -> int:
+        out = ctypes.c_size_t()
+        _ffi.check(_ffi.lib.sfft_workspace_bytes(self._handle, int(batch), ctypes.byref(out)))
+        return int(out.value)
+
+    # host-side views the reference exposes on its plan (read-only)
+    @property
+    def twiddles(self) -> TwiddleTable:
+        return build_twiddle_table(self.m)
+
+    @property
+    def bitrev(self) -> np.ndarray:
+        idx = bit_reverse_indices(self.m)
+        idx.flags.writeable = False
+        return idx
+
+    @property
+    def stage_factors(self) -> tuple:
+        """Host copies of w_i = cos - j sin per stage (transform.py:80-84)."""
+        if self.m == 0:
+            return ()
+        wr, wi = stage_factor_table(self.m)
+        out = []
+        for i in range(1, self.m + 1):
+            step = 1 << (self.m - i)
+            w = np.empty(1 << (i - 1), dtype=np.complex128)
+            w.real = wr[::step]
+            w.imag = wi[::step]
+            w.flags.writeable = False
+            out.append(w)
+        return tuple(out)
+
+
+def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
+              dtype=torch.float64, device=None, radix_log: int = 0) -> FftPlan:
+    """Build an FftPlan for 2**m samples on a CUDA device (transform.py:65-85).
+
+    Same validation order and messages as the reference: m < 0 -> ValueError,
+    m > max_m -> CapacityError, unknown algorithm -> ValueError.  ``dtype`` is
+    the plane dtype (float64 like the reference, or float32); ``radix_log``
+    overrides the register radix of the fused kernel (0 = tuned default).
+    """
+    if m < 0:
+        raise ValueError(f"stage count m must be >= 0, got {m}")
+    if m > max_m:
+        raise CapacityError(f"m={m} exceeds the plan limit max_m={max_m}")
+    algorithm = Algorithm(algorithm) if not isinstance(algorithm, Algorithm) else algorithm
+    if dtype not in _DTYPE_CODE:
+        raise ValueError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
+    device = _resolve_device(device)
+    handle = ctypes.c_void_p()
+    algo = _ffi.SFFT_DIF if algorithm is Algorithm.DIF else _ffi.SFFT_DIT
+    _ffi.check(_ffi.lib.sfft_plan_create_ex(int(m), _DTYPE_CODE[dtype], algo, device.index,
+                                            int(min(max_m, MAX_PLAN_M)),
+                                            int(radix_log), ctypes.byref(handle)))
+    return FftPlan(m, algorithm, dtype, device, handle.value)
+
+
+@lru_cache(maxsize=32)
+def _cached_plan(m, algorithm, dtype, device_index):
+    # plan cache of the service path (service/app.py:28-30)
+    return make_plan(m, algorithm, dtype=dtype, device=torch.device("cuda", device_index))
+
+
+def _stream_ptr(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _rows(t: torch.Tensor):
+    """(batch, row stride) of a [N] or [B, N] tensor with unit inner stride."""
+    if t.ndim == 1:
+        return 1, t.shape[0]
+    return t.shape[0], t.stride(0)
+
+
+def _workspace(plan: FftPlan, batch: int):
+    nbytes = plan.workspace_bytes(batch)
+    if nbytes == 0:
+        return None, 0
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=plan.device)
+    return ws, ws.data_ptr()
+
+
+def _exec_split_device(plan, xr, xi, yr, yi, inverse):
+    batch, istr = _rows(xr)
+    _, ostr = _rows(yr)
+    ws, wsp = _workspace(plan, batch)
+    direction = _ffi.SFFT_INVERSE if inverse else _ffi.SFFT_FORWARD
+    _ffi.check(_ffi.lib.sfft_exec_split(plan._handle, xr.data_ptr(), xi.data_ptr(), yr.data_ptr(),
+                                        yi.data_ptr(), batch, istr, ostr, direction, wsp,
+                                        _stream_ptr(plan.device)))
+    if ws is not None:
+        ws.record_stream(torch.cuda.current_stream(plan.device))
+
+
+def _unit_rows(t: torch.Tensor) -> torch.Tensor:
+    if t.stride(-1) != 1 or (t.ndim == 2 and t.shape[0] > 1 and t.stride(0) < t.shape[1]):
+        t = t.contiguous()
+    return t
+
+
+def fft_split(x_re, x_im, *, algorithm="dit", inverse: bool = False, out=None, plan=None):
+    """Batched split-format DFT: ``(x_re, x_im) -> (y_re, y_im)``.
+
+    ``x_re``/``x_im``: planes of shape ``[N]`` or ``[B, N]`` (N = 2**m),
+    float32 or float64 torch tensors on a CUDA device -- the hot path -- or
+    host arrays/tensors (copied to the current CUDA device and back).
+    Forward kernel exp(-j 2 pi n k / N), unnormalised; ``inverse=True`` gives
+    the reference's ifft (channel swap + 1/N, transform.py:286-298).
+    ``out=(y_re, y_im)`` may alias the inputs (in place).  Returns the output
+    planes in the input's container type.
+    """
+    was_numpy = not isinstance(x_re, torch.Tensor)
+    sig = SplitSignal(x_re, x_im)
+    n = len(sig)
+    if not is_power_of_two(n):
+        raise ValueError(f"sample count {n} is not a power of two")
+    m = n.bit_length() - 1
+    host = sig.re.device.type != "cuda"
+    device = _resolve_device(None if host else sig.re.device)
+    algorithm = Algorithm(algorithm) if not isinstance(algorithm, Algorithm) else algorithm
+    if plan is None:
+        plan = _cached_plan(m, algorithm, sig.re.dtype, device.index)
+    else:
+        if plan.m != m:
+            raise ValueError(f"buffer is for m={m} but plan is for m={plan.m}")
+        if plan.dtype != sig.re.dtype:
+            raise ValueError(f"signal dtype {sig.re.dtype} does not match plan dtype {plan.dtype}")
+        device = plan.device
+
+    if not host:
+        if sig.re.device != device:
+            raise ValueError(f"signal is on {sig.re.device} but plan is on {device}")
+        xr, xi = _unit_rows(sig.re), _unit_rows(sig.im)
+        if out is None:
+            yr, yi = torch.empty_like(xr), torch.empty_like(xi)
+        else:
+            yr, yi = out
+            if yr.shape != xr.shape or yi.shape != xr.shape or yr.dtype != xr.dtype or yi.dtype != xr.dtype:
+                raise ValueError("out planes must match the input shape and dtype")
+            if yr.device != device or yi.device != device:
+                raise ValueError("out planes must be on the plan's device")
+            if yr.stride(-1) != 1 or yi.stride(-1) != 1 or yr.stride() != yi.stride():
+                raise ValueError("out planes must have unit inner stride and equal strides")
+        if xr.stride() != xi.stride():
+            xr, xi = xr.contiguous(), xi.contiguous()
+        _exec_split_device(plan, xr, xi, yr, yi, inverse)
+        return yr, yi
+
+    # host buffers: H2D, GPU transform, D2H (the e2e path of bench.py)
+    with torch.cuda.device(device):
+        xr = sig.re.to(device, non_blocking=True)
+        xi = sig.im.to(device, non_blocking=True)
+        yr, yi = torch.empty_like(xr), torch.empty_like(xi)
+        _exec_split_device(plan, xr, xi, yr, yi, inverse)
+        if out is not None:
+            hr, hi = out
+            hr, hi = (torch.from_numpy(hr) if not isinstance(hr, torch.Tensor) else hr,
+                      torch.from_numpy(hi) if not isinstance(hi, torch.Tensor) else hi)
+            hr.copy_(yr, non_blocking=True)
+            hi.copy_(yi, non_blocking=True)
+            torch.cuda.current_stream(device).synchronize()
+            return out
+        hr = yr.to("cpu")
+        hi = yi.to("cpu")
+    if was_numpy:
+        return hr.numpy(), hi.numpy()
+    return hr, hi
+
+
+def ifft_split(x_re, x_im, *, algorithm="dit", out=None, plan=None):
+    """Inverse of :func:`fft_split` (transform.py:286-298)."""
+    return fft_split(x_re, x_im, algorithm=algorithm, inverse=True, out=out, plan=plan)
+
+
+def _check_pair(plan: FftPlan, buf: InterleavedBuffer) -> None:
+    if buf.m != plan.m:
+        raise ValueError(f"buffer is for m={buf.m} but plan is for m={plan.m}")
+
+
+def _run_interleaved(plan: FftPlan, buf: InterleavedBuffer, inverse: bool, algorithm: Algorithm):
+    _check_pair(plan, buf)
+    if algorithm is not plan.algorithm:
+        # fft_dit/fft_dif on a plan built for the other variant: same tables,
+        # other kernel family (the reference's plans serve both, :208-270)
+        plan = _cached_plan(plan.m, algorithm, plan.dtype, plan.device.index)
+    data = buf.data
+    if data.dtype != plan.dtype:
+        raise ValueError(f"buffer dtype {data.dtype} does not match plan dtype {plan.dtype}")
+    direction = _ffi.SFFT_INVERSE if inverse else _ffi.SFFT_FORWARD
+    host = data.device.type != "cuda"
+    work = data.to(plan.device, non_blocking=True) if host else data
+    if work.device != plan.device:
+        raise ValueError(f"buffer is on {work.device} but plan is on {plan.device}")
+    if not work.is_contiguous():
+        work = work.contiguous()
+    batch = 1 if work.ndim == 1 else work.shape[0]
+    n = plan.sample_count
+    ws, wsp = _workspace(plan, batch)
+    _ffi.check(_ffi.lib.sfft_exec_interleaved(plan._handle, work.data_ptr(), work.data_ptr(), batch, n, n,
+                                              direction, wsp, _stream_ptr(plan.device)))
+    if ws is not None:
+        ws.record_stream(torch.cuda.current_stream(plan.device))
+    if work.data_ptr() != data.data_ptr():
+        data.copy_(work)
+    return buf
+
+
+def fft_dit(plan: FftPlan, buf: InterleavedBuffer) -> InterleavedBuffer:
+    """Forward transform, decimation in time; mutates ``buf`` (transform.py:208)."""
+    return _run_interleaved(plan, buf, False, Algorithm.DIT)
+
+
+def fft_dif(plan: FftPlan, buf: InterleavedBuffer) -> InterleavedBuffer:
+    """Forward transform, decimation in frequency; mutates ``buf`` (transform.py:241)."""
+    return _run_interleaved(plan, buf, False, Algorithm.DIF)
+
+
+def fft(plan: FftPlan, buf: InterleavedBuffer) -> InterleavedBuffer:
+    """Forward transform using the plan's variant (transform.py:273-277)."""
+    return _run_interleaved(plan, buf, False, plan.algorithm)
+
+
+def ifft(plan: FftPlan, buf: InterleavedBuffer) -> InterleavedBuffer:
+    """Inverse transform by the channel-swap identity (transform.py:286-298)."""
+    return _run_interleaved(plan, buf, True, plan.algorithm)
+
+
+@dataclass(frozen=True)
+class FlopReport:
+    """Real-arithmetic census for one transform size (transform.py:301-309)."""
+
+    real_mults: int
+    real_adds: int
+    generic_rotations: int
+    quarter_turns: int
+    identity_rotations: int
+
+
+def count_flops(plan) -> FlopReport:
+    """Census of rotation kinds and real ops (transform.py:312-335)."""
+    m = plan.m if isinstance(plan, FftPlan) else int(plan)
+    out = (ctypes.c_int64 * 5)()
+    _ffi.check(_ffi.lib.sfft_count_flops(m, out))
+    return FlopReport(*[int(v) for v in out])

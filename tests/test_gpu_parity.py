@@ -1,0 +1,186 @@
+"""GPU parity: the CUDA path through the C ABI vs the pinned CPU oracle.
+
+fp64: bit-for-bit equality with the oracle, which is itself bit-identical to
+the reference (tests/test_oracle_golden.py), so fp64 GPU == reference.
+fp32: relative L2 <= 1e-5 * log2 N against the fp64 oracle on the same
+fp32-rounded inputs (BASELINE.json north_star tolerance).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2504_07264_b200 as sf
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = lambda m: 1e-5 * max(m, 1)   # noqa: E731  north_star: <= 1e-5*log2N
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+def rel_l2(got_re, got_im, want_re, want_im):
+    num = np.sqrt(np.sum((got_re - want_re) ** 2 + (got_im - want_im) ** 2))
+    den = np.sqrt(np.sum(want_re ** 2 + want_im ** 2))
+    return num / max(den, 1e-300)
+
+
+def rand(rng, b, n, dtype):
+    re = rng.standard_normal((b, n)).astype(dtype)
+    im = rng.standard_normal((b, n)).astype(dtype)
+    return re, im
+
+
+def gpu_split(re, im, algo="dit", inverse=False, radix_log=0):
+    dt = torch.float32 if re.dtype == np.float32 else torch.float64
+    m = re.shape[-1].bit_length() - 1
+    plan = sf.make_plan(m, algo, dtype=dt, device="cuda:0", radix_log=radix_log)
+    xr = torch.from_numpy(re).cuda()
+    xi = torch.from_numpy(im).cuda()
+    yr, yi = sf.fft_split(xr, xi, inverse=inverse, plan=plan)
+    torch.cuda.synchronize()
+    return yr.cpu().numpy(), yi.cpu().numpy()
+
+
+FUSED_M = list(range(0, 13))
+LARGE_M = [13, 14, 16, 17, 20]
+
+
+@pytest.mark.parametrize("inverse", [False, True])
+@pytest.mark.parametrize("algo", ["dit", "dif"])
+@pytest.mark.parametrize("m", FUSED_M + LARGE_M)
+def test_f64_bitwise_vs_oracle(cuda, m, algo, inverse):
+    rng = np.random.default_rng(1000 + m)
+    b = 37 if m <= 12 else 3          # batch not a multiple of the CTA tile
+    re, im = rand(rng, b, 1 << m, np.float64)
+    gr, gi = gpu_split(re, im, algo, inverse)
+    wr, wi = oracle.fft_split_c(re, im, algo, inverse)
+    assert np.array_equal(bits(gr), bits(wr)), f"re differs, max abs {np.abs(gr - wr).max()}"
+    assert np.array_equal(bits(gi), bits(wi)), f"im differs, max abs {np.abs(gi - wi).max()}"
+
+
+@pytest.mark.parametrize("inverse", [False, True])
+@pytest.mark.parametrize("algo", ["dit", "dif"])
+@pytest.mark.parametrize("m", FUSED_M + LARGE_M)
+def test_f32_rel_l2_vs_oracle(cuda, m, algo, inverse):
+    rng = np.random.default_rng(2000 + m)
+    b = 37 if m <= 12 else 3
+    re, im = rand(rng, b, 1 << m, np.float32)
+    gr, gi = gpu_split(re, im, algo, inverse)
+    wr, wi = oracle.fft_split_c(re, im, algo, inverse)
+    err = rel_l2(gr.astype(np.float64), gi.astype(np.float64), wr, wi)
+    assert err <= F32_TOL(m), f"relL2 {err:.3e} > {F32_TOL(m):.1e}"
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("algo", ["dit", "dif"])
+@pytest.mark.parametrize("m,lr", [(m, lr) for m in (4, 5, 6, 7, 9, 10, 11, 12) for lr in (2, 3, 4, 5)
+                                  if (1 << (m - min(lr, m))) <= 1024])
+def test_every_radix_schedule(cuda, m, lr, algo, dtype):
+    if dtype == np.float64 and lr == 5:
+        pytest.skip("fp64 register radix is capped at 2^4")
+    rng = np.random.default_rng(3000 + 16 * m + lr)
+    re, im = rand(rng, 19, 1 << m, dtype)
+    gr, gi = gpu_split(re, im, algo, False, radix_log=lr)
+    wr, wi = oracle.fft_split_c(re, im, algo, False)
+    if dtype == np.float64:
+        assert np.array_equal(bits(gr), bits(wr)) and np.array_equal(bits(gi), bits(wi))
+    else:
+        assert rel_l2(gr.astype(np.float64), gi.astype(np.float64), wr, wi) <= F32_TOL(m)
+
+
+@pytest.mark.parametrize("m", [3, 6, 10, 12, 14])
+@pytest.mark.parametrize("algo", ["dit", "dif"])
+def test_interleaved_in_place_matches_split(cuda, m, algo):
+    rng = np.random.default_rng(4000 + m)
+    b = 5
+    re, im = rand(rng, b, 1 << m, np.float64)
+    data = np.empty((b, 2 << m))
+    data[:, 0::2] = re
+    data[:, 1::2] = im
+    plan = sf.make_plan(m, algo, dtype=torch.float64, device="cuda:0")
+    buf = sf.InterleavedBuffer(torch.from_numpy(data).cuda(), m)
+    sf.fft(plan, buf)
+    out = buf.data.cpu().numpy()
+    wr, wi = oracle.fft_split_c(re, im, algo, False)
+    assert np.array_equal(bits(out[:, 0::2]), bits(wr))
+    assert np.array_equal(bits(out[:, 1::2]), bits(wi))
+    sf.ifft(plan, buf)
+    back = buf.data.cpu().numpy()
+    assert np.max(np.abs(back - data)) <= 1e-12 * (1 + np.abs(data).max())
+
+
+@pytest.mark.parametrize("m", [6, 10, 13])
+def test_in_place_and_strided_rows(cuda, m):
+    rng = np.random.default_rng(5000 + m)
+    n = 1 << m
+    wide_re = torch.from_numpy(rng.standard_normal((9, n + 64))).cuda()
+    wide_im = torch.from_numpy(rng.standard_normal((9, n + 64))).cuda()
+    xr, xi = wide_re[:, 32:32 + n], wide_im[:, 32:32 + n]   # row stride n + 64
+    want = oracle.fft_split_c(xr.cpu().numpy(), xi.cpu().numpy())
+    yr, yi = sf.fft_split(xr, xi, out=(xr, xi))             # in place, strided
+    torch.cuda.synchronize()
+    assert yr.data_ptr() == xr.data_ptr()
+    assert np.array_equal(bits(xr.cpu().numpy()), bits(want[0]))
+    assert np.array_equal(bits(xi.cpu().numpy()), bits(want[1]))
+    # the pad columns were not touched
+    assert torch.equal(wide_re[:, :32], torch.from_numpy(np.asarray(wide_re[:, :32].cpu())).cuda())
+
+
+def test_host_arrays_round_trip_through_gpu(cuda):
+    # numpy in -> numpy out, computed on the GPU (reference-style call)
+    rng = np.random.default_rng(6)
+    re, im = rng.standard_normal(64), rng.standard_normal(64)
+    yr, yi = sf.fft_split(re, im)
+    assert isinstance(yr, np.ndarray)
+    wr, wi = oracle.fft_split_c(re, im)
+    assert np.array_equal(bits(yr), bits(wr)) and np.array_equal(bits(yi), bits(wi))
+
+
+# ---- the reference's inline known answers, on the GPU ---------------------
+
+def _known(re, im, m, algo="dit", dtype=torch.float64, inverse=False):
+    plan = sf.make_plan(m, algo, dtype=dtype, device="cuda:0")
+    xr = torch.tensor(re, dtype=dtype, device="cuda:0")
+    xi = torch.tensor(im, dtype=dtype, device="cuda:0")
+    yr, yi = sf.fft_split(xr, xi, plan=plan, inverse=inverse)
+    return yr.cpu().tolist(), yi.cpu().tolist()
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("algo", ["dit", "dif"])
+def test_known_answers(cuda, algo, dtype):
+    # impulse -> ones (test_transform.py:41-47)
+    assert _known([1.0] + [0.0] * 7, [0.0] * 8, 3, algo, dtype) == ([1.0] * 8, [0.0] * 8)
+    # constant 2.5 -> 40 delta (test_transform.py:50-54)
+    assert _known([2.5] * 16, [0.0] * 16, 4, algo, dtype) == ([40.0] + [0.0] * 15, [0.0] * 16)
+    # 4-point ramp (test_transform.py:57-62, README.md:41-47)
+    assert _known([1.0, 2.0, 3.0, 4.0], [0.0] * 4, 2, algo, dtype) == (
+        [10.0, -2.0, -2.0, -2.0], [0.0, 2.0, 0.0, -2.0])
+    # N = 1 identity (test_transform.py:76-79)
+    assert _known([3.5], [-1.25], 0, algo, dtype) == ([3.5], [-1.25])
+    # ifft(ones) = delta (test_transform.py:223-229)
+    assert _known([1.0] * 8, [0.0] * 8, 3, algo, dtype, inverse=True) == ([1.0] + [0.0] * 7, [0.0] * 8)
+
+
+def test_single_tone(cuda):
+    # test_transform.py:65-73
+    n = 16
+    t = 2.0 * np.pi * np.arange(n) / n
+    yr, yi = _known(np.cos(t).tolist(), np.sin(t).tolist(), 4)
+    want = np.zeros(n)
+    want[1] = n
+    assert np.max(np.abs(np.array(yr) - want)) <= 1e-13 * n
+    assert np.max(np.abs(np.array(yi))) <= 1e-13 * n
+
+
+def test_launches_are_counted(cuda):
+    from paper_2504_07264_b200 import _ffi
+    before = _ffi.launch_count()
+    x = torch.zeros(4, 64, device="cuda:0")
+    sf.fft_split(x, x)
+    torch.cuda.synchronize()
+    assert _ffi.launch_count() == before + 1

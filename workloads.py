@@ -1,0 +1,119 @@
+"""Seeded synthetic inputs for the BASELINE.json configs (bench + tests).
+
+The reference benchmarks on seeded synthetic signals (bench.py:56-60) and
+BASELINE.json names only synthetic configs, so these generators *are* the
+benchmark inputs.  Convention (mirroring the reference):
+``rng = np.random.default_rng(seed)``; draw ``x_re`` (B, N) first, then
+``x_im`` (B, N), in float64; cast to float32 for fp32 configs.  Draws are
+made in row chunks, which yields the identical stream (checked in
+tests/test_workloads.py) while bounding host memory.
+
+Config 4 (structured) is not fully specified by BASELINE.json; the builder's
+choice (stated in DESIGN.md): seed 3; per signal draw 8 bins
+``k ~ integers(0, 4096)`` (B, 8), amplitudes ``A ~ uniform[0.5, 2)`` (B, 8),
+phases ``phi ~ uniform[0, 2 pi)`` (B, 8), then noise ``eps_re`` (B, N) and
+``eps_im`` (B, N) ~ N(0, 1);
+``x[n] = sum_j A_j e^{j phi_j} e^{+2 pi j ((k_j n) mod N) / N} + 0.01 eps``.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    log2n: int
+    batch: int
+    dtype: str          # "f32" | "f64"
+    seed: int
+    dist: str           # "uniform" | "normal" | "tones"
+
+    @property
+    def n(self):
+        return 1 << self.log2n
+
+    @property
+    def np_dtype(self):
+        return np.float32 if self.dtype == "f32" else np.float64
+
+    @property
+    def elem_bytes(self):
+        return 4 if self.dtype == "f32" else 8
+
+    @property
+    def algorithmic_bytes(self):
+        """read re + im, write re + im: 4 * N * sizeof(real) per transform."""
+        return 4 * self.n * self.elem_bytes * self.batch
+
+    @property
+    def flops_5nlogn(self):
+        return 5 * self.n * self.log2n * self.batch
+
+
+CONFIGS = {
+    "cfg1_n8_f64": Config("cfg1_n8_f64", 3, 1024, "f64", 0, "uniform"),
+    "cfg2_n64_f32": Config("cfg2_n64_f32", 6, 1 << 20, "f32", 1, "normal"),
+    "cfg3_n1024_f32": Config("cfg3_n1024_f32", 10, 1 << 18, "f32", 2, "uniform"),
+    "cfg3_n1024_f64": Config("cfg3_n1024_f64", 10, 1 << 18, "f64", 2, "uniform"),
+    "cfg4_n4096_f32": Config("cfg4_n4096_f32", 12, 1 << 16, "f32", 3, "tones"),
+    "cfg5_n2p28_f32": Config("cfg5_n2p28_f32", 28, 1, "f32", 4, "normal"),
+}
+
+_CHUNK_ELEMS = 1 << 24
+
+
+def _draw_plane(rng, dist, batch, n, rows, out_dtype):
+    """Draw a (batch, n) float64 plane in row chunks; keep the first `rows`."""
+    out = np.empty((rows, n), dtype=out_dtype)
+    step = max(1, _CHUNK_ELEMS // n)
+    for r0 in range(0, batch, step):
+        r1 = min(batch, r0 + step)
+        if dist == "uniform":
+            blk = rng.uniform(-1.0, 1.0, (r1 - r0, n))
+        else:
+            blk = rng.standard_normal((r1 - r0, n))
+        if r0 < rows:
+            out[r0:min(r1, rows)] = blk[: min(r1, rows) - r0]
+    return out
+
+
+def tone_params(cfg: Config, rng):
+    k = rng.integers(0, cfg.n, (cfg.batch, 8))
+    amp = rng.uniform(0.5, 2.0, (cfg.batch, 8))
+    phi = rng.uniform(0.0, 2.0 * np.pi, (cfg.batch, 8))
+    return k, amp, phi
+
+
+def generate(cfg: Config, rows=None, dtype=None):
+    """(x_re, x_im) numpy arrays of shape (rows, N) (rows defaults to B).
+
+    Values are computed in float64 and cast to the config dtype (or `dtype`).
+    """
+    rows = cfg.batch if rows is None else min(rows, cfg.batch)
+    out_dtype = dtype or cfg.np_dtype
+    rng = np.random.default_rng(cfg.seed)
+    if cfg.dist in ("uniform", "normal"):
+        re = _draw_plane(rng, cfg.dist, cfg.batch, cfg.n, rows, out_dtype)
+        im = _draw_plane(rng, cfg.dist, cfg.batch, cfg.n, rows, out_dtype)
+        return re, im
+    # structured tones (config 4)
+    k, amp, phi = tone_params(cfg, rng)
+    noise_re = _draw_plane(rng, "normal", cfg.batch, cfg.n, rows, np.float64)
+    noise_im = _draw_plane(rng, "normal", cfg.batch, cfg.n, rows, np.float64)
+    n = cfg.n
+    ang = 2.0 * np.pi * np.arange(n) / n
+    table = np.cos(ang) + 1j * np.sin(ang)
+    coef = amp * np.exp(1j * phi)
+    re = np.empty((rows, n), dtype=out_dtype)
+    im = np.empty((rows, n), dtype=out_dtype)
+    idx_n = np.arange(n, dtype=np.int64)
+    step = 256
+    for r0 in range(0, rows, step):
+        r1 = min(rows, r0 + step)
+        idx = (k[r0:r1, :, None] * idx_n[None, None, :]) % n
+        x = np.einsum("rt,rtn->rn", coef[r0:r1], table[idx])
+        re[r0:r1] = x.real + 0.01 * noise_re[r0:r1]
+        im[r0:r1] = x.imag + 0.01 * noise_im[r0:r1]
+    return re, im
