@@ -1,0 +1,53 @@
+"""The C-ABI library loads without a GPU and exports every declared symbol."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+
+from paper_2504_07264_b200 import _ffi
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "splitfft_b200.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(sfft_\w+)\s*\(", text)))
+
+
+def test_header_declares_the_expected_entry_points():
+    syms = declared_symbols()
+    for name in ("sfft_plan_create", "sfft_plan_destroy", "sfft_exec_split", "sfft_exec_interleaved",
+                 "sfft_workspace_bytes", "sfft_last_error", "sfft_abi_version"):
+        assert name in syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_ffi.LIB_PATH)
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, f"not exported: {missing}"
+    assert set(declared_symbols()) == set(_ffi.SIGNATURES), "ctypes table out of sync with the header"
+
+
+def test_abi_version_and_error_reporting():
+    assert _ffi.lib.sfft_abi_version() == _ffi.ABI_VERSION
+    wr = np.zeros(4)
+    assert _ffi.lib.sfft_twiddle_table(0, wr.ctypes.data, wr.ctypes.data) == _ffi.SFFT_EINVAL
+    assert b"log2n" in _ffi.lib.sfft_last_error()
+
+
+def test_plan_create_validates_before_touching_the_device():
+    h = ctypes.c_void_p()
+    assert _ffi.lib.sfft_plan_create(-1, 0, 0, 0, 30, ctypes.byref(h)) == _ffi.SFFT_EINVAL
+    assert b"must be >= 0" in _ffi.lib.sfft_last_error()
+    assert _ffi.lib.sfft_plan_create(12, 0, 0, 0, 10, ctypes.byref(h)) == _ffi.SFFT_ECAPACITY
+    assert b"exceeds the plan limit" in _ffi.lib.sfft_last_error()
+    assert _ffi.lib.sfft_plan_create(5, 0, 7, 0, 30, ctypes.byref(h)) == _ffi.SFFT_EINVAL
+    assert _ffi.lib.sfft_exec_split(None, None, None, None, None, 1, 8, 8, -1, None, None) == _ffi.SFFT_EINVAL
+
+
+def test_launch_counter_is_exported():
+    assert _ffi.launch_count() >= 0
