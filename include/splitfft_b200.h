@@ -50,6 +50,12 @@ extern "C" {
 #define SFFT_FORWARD (-1)
 #define SFFT_INVERSE (+1)
 
+/* kernel family of the fused (log2n <= 12) path */
+#define SFFT_KERNEL_AUTO 0  /* TMA-fed persistent kernel when the rows allow it, else LDG/STG */
+#define SFFT_KERNEL_LDG 1   /* per-thread global loads/stores (any stride/alignment, interleaved) */
+#define SFFT_KERNEL_TMA 2   /* require the TMA kernel (planar, 16-byte aligned rows and strides) */
+#define SFFT_KERNEL_PASS 3  /* reported by sfft_plan_info for the multi-launch path (log2n > 12) */
+
 /* plan limit, transform.py:32 (MAX_PLAN_M) */
 #define SFFT_MAX_LOG2N 30
 
@@ -70,18 +76,20 @@ const char *sfft_last_error(void);
 int sfft_plan_create(int log2n, int dtype, int algorithm, int device,
                      int max_log2n, sfft_plan **out);
 
-/* Same, with an explicit radix schedule: log2 of the register radix used by
- * each fused pass (0 = library default).  Used by the tuner and tests. */
+/* Same, with an explicit register radix (log2; 0 = tuned default) and
+ * kernel family (SFFT_KERNEL_*).  Used by the tuner and the tests. */
 int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device,
-                        int max_log2n, int log2_radix, sfft_plan **out);
+                        int max_log2n, int log2_radix, int kernel,
+                        sfft_plan **out);
 
 int sfft_plan_destroy(sfft_plan *plan);
 
 /* Plan introspection: log2n, dtype, algorithm, device, number of kernel
- * launches per exec, register radix (log2).  Any pointer may be NULL. */
+ * launches per exec, register radix (log2), kernel family used for aligned
+ * planar rows (SFFT_KERNEL_*).  Any pointer may be NULL. */
 int sfft_plan_info(const sfft_plan *plan, int *log2n, int *dtype,
                    int *algorithm, int *device, int *launches_per_exec,
-                   int *log2_radix);
+                   int *log2_radix, int *kernel);
 
 /* Bytes of device workspace exec needs for `batch` rows (0 for the fused
  * single-kernel path, log2n <= 12). */

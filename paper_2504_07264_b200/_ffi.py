@@ -18,6 +18,7 @@ SFFT_F32, SFFT_F64 = 0, 1
 SFFT_DIT, SFFT_DIF = 0, 1
 SFFT_FORWARD, SFFT_INVERSE = -1, 1
 SFFT_MAX_LOG2N = 30
+SFFT_KERNEL_AUTO, SFFT_KERNEL_LDG, SFFT_KERNEL_TMA, SFFT_KERNEL_PASS = 0, 1, 2, 3
 ABI_VERSION = 1
 
 # every symbol include/splitfft_b200.h declares: name -> (restype, argtypes)
@@ -28,9 +29,9 @@ SIGNATURES = {
     "sfft_abi_version": (_I, []),
     "sfft_last_error": (ctypes.c_char_p, []),
     "sfft_plan_create": (_I, [_I, _I, _I, _I, _I, ctypes.POINTER(_P)]),
-    "sfft_plan_create_ex": (_I, [_I, _I, _I, _I, _I, _I, ctypes.POINTER(_P)]),
+    "sfft_plan_create_ex": (_I, [_I, _I, _I, _I, _I, _I, _I, ctypes.POINTER(_P)]),
     "sfft_plan_destroy": (_I, [_P]),
-    "sfft_plan_info": (_I, [_P] + [ctypes.POINTER(_I)] * 6),
+    "sfft_plan_info": (_I, [_P] + [ctypes.POINTER(_I)] * 7),
     "sfft_workspace_bytes": (_I, [_P, _I64, ctypes.POINTER(ctypes.c_size_t)]),
     "sfft_exec_split": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I, _P, _P]),
     "sfft_exec_interleaved": (_I, [_P, _P, _P, _I64, _I64, _I64, _I, _P, _P]),

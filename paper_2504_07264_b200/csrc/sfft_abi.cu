@@ -20,10 +20,27 @@
 #include "sfft_fused.cuh"
 #include "sfft_launch.h"
 #include "sfft_pass.cuh"
+#include "sfft_tma_host.h"
+
+#include <mutex>
 
 namespace sfft {
 static std::atomic<int64_t> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder()
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
 }  // namespace sfft
 
 using namespace sfft;
@@ -111,6 +128,9 @@ struct Group {
 
 struct sfft_plan {
     int log2n = 0, dtype = 0, algo = 0, device = 0, lr = 0;
+    int kernel = SFFT_KERNEL_AUTO;  // fused-path kernel family
+    int lr_tma = -1;                // radix of the TMA kernel (-1: none)
+    int lr_ldg_il = 0;              // radix of the interleaved LDG kernel
     // fused path
     void *d_tw = nullptr;          // vec2_t<T> table of stage tw_top
     int tw_top = 0;
@@ -218,8 +238,35 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     const double scale = inv ? 1.0 / (double)(int64_t(1) << m) : 1.0;
 
     if (m <= kFusedMaxLog) {
-        FusedLaunchFn fn = fused_launcher_algo(p->dtype, m, p->lr, p->algo == SFFT_DIF, il);
-        if (!fn) return fail(SFFT_EINVAL, "no fused kernel for log2n=%d radix=2^%d layout=%s", m, p->lr,
+        const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
+        const bool aligned = ((uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)y0 | (uintptr_t)y1) % 16 == 0 &&
+                             ((size_t)is * esz) % 16 == 0 && ((size_t)os * esz) % 16 == 0 &&
+                             batch < (int64_t(1) << 31);
+        if (!il && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG && aligned) {
+            TmaLaunchFn tf = tma_launcher(p->dtype, m, p->lr_tma, p->algo == SFFT_DIF);
+            if (tf) {
+                TmaLaunch L;
+                L.x_re = x0;
+                L.x_im = x1;
+                L.y_re = y0;
+                L.y_im = y1;
+                L.batch = batch;
+                L.in_stride = batch > 1 ? is : (int64_t(1) << m);
+                L.out_stride = batch > 1 ? os : (int64_t(1) << m);
+                L.inverse = inv ? 1 : 0;
+                L.scale = scale;
+                L.tw = p->d_tw;
+                cudaError_t e = tf(L, st);
+                if (e != cudaSuccess) return cuda_fail(e, "TMA kernel launch");
+                return SFFT_OK;
+            }
+        }
+        if (p->kernel == SFFT_KERNEL_TMA)
+            return fail(SFFT_EINVAL, "the TMA kernel needs planar, 16-byte aligned rows with 16-byte row strides "
+                                     "and a size with a TMA configuration (log2n=%d)", m);
+        const int lr = il ? p->lr_ldg_il : p->lr;
+        FusedLaunchFn fn = fused_launcher_algo(p->dtype, m, lr, p->algo == SFFT_DIF, il);
+        if (!fn) return fail(SFFT_EINVAL, "no fused kernel for log2n=%d radix=2^%d layout=%s", m, lr,
                              il ? "interleaved" : "planar");
         FusedArgs a;
         a.x0 = x0;
@@ -328,7 +375,7 @@ int sfft_count_flops(int log2n, int64_t *out5)
 }
 
 int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max_log2n, int log2_radix,
-                        sfft_plan **out)
+                        int kernel, sfft_plan **out)
 {
     if (!out) return fail(SFFT_EINVAL, "out is NULL");
     *out = nullptr;
@@ -340,6 +387,8 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
     if (algorithm != SFFT_DIT && algorithm != SFFT_DIF)
         return fail(SFFT_EINVAL, "%d is not a valid Algorithm (0 = dit, 1 = dif)", algorithm);
     if (dtype != SFFT_F32 && dtype != SFFT_F64) return fail(SFFT_EINVAL, "unknown dtype %d", dtype);
+    if (kernel != SFFT_KERNEL_AUTO && kernel != SFFT_KERNEL_LDG && kernel != SFFT_KERNEL_TMA)
+        return fail(SFFT_EINVAL, "unknown kernel family %d", kernel);
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
@@ -356,8 +405,11 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
         return cuda_fail(dg.err, "cudaSetDevice");
     }
     int rc = SFFT_OK;
+    p->kernel = kernel;
     if (log2n <= kFusedMaxLog) {
-        int lr = log2_radix > 0 ? log2_radix : fused_default_lr(dtype, log2n);
+        const int tma_lr = tma_default_lr(dtype, log2n);
+        int lr = log2_radix > 0 ? log2_radix
+                                : (kernel != SFFT_KERNEL_LDG && tma_lr >= 0 ? tma_lr : fused_default_lr(dtype, log2n));
         if (log2n == 0) lr = 0;
         if (lr > log2n) lr = log2n;
         if (!fused_launcher_algo(dtype, log2n, lr, algorithm == SFFT_DIF, false)) {
@@ -365,6 +417,12 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
             return fail(SFFT_EINVAL, "radix 2^%d is not available for log2n=%d", lr, log2n);
         }
         p->lr = lr;
+        p->lr_ldg_il = fused_default_lr(dtype, log2n);
+        if (kernel != SFFT_KERNEL_LDG && tma_launcher(dtype, log2n, lr, false)) p->lr_tma = lr;
+        if (kernel == SFFT_KERNEL_TMA && p->lr_tma < 0) {
+            delete p;
+            return fail(SFFT_EINVAL, "no TMA kernel for log2n=%d radix=2^%d", log2n, lr);
+        }
         rc = dtype == SFFT_F32 ? upload_table<float>(p, log2n) : upload_table<double>(p, log2n);
     } else {
         p->lr = pass_default_lr(dtype);
@@ -386,7 +444,7 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
 
 int sfft_plan_create(int log2n, int dtype, int algorithm, int device, int max_log2n, sfft_plan **out)
 {
-    return sfft_plan_create_ex(log2n, dtype, algorithm, device, max_log2n, 0, out);
+    return sfft_plan_create_ex(log2n, dtype, algorithm, device, max_log2n, 0, SFFT_KERNEL_AUTO, out);
 }
 
 int sfft_plan_destroy(sfft_plan *plan)
@@ -398,8 +456,9 @@ int sfft_plan_destroy(sfft_plan *plan)
 }
 
 int sfft_plan_info(const sfft_plan *p, int *log2n, int *dtype, int *algorithm, int *device, int *launches,
-                   int *log2_radix)
+                   int *log2_radix, int *kernel)
 {
+    if (kernel && p) *kernel = p->lr_tma >= 0 ? SFFT_KERNEL_TMA : (p->log2n <= kFusedMaxLog ? SFFT_KERNEL_LDG : SFFT_KERNEL_PASS);
     if (!p) return fail(SFFT_EINVAL, "plan is NULL");
     if (log2n) *log2n = p->log2n;
     if (dtype) *dtype = p->dtype;

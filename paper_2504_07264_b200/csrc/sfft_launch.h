@@ -8,12 +8,16 @@ namespace sfft {
 
 struct FusedArgs;
 struct PassArgs;
+struct TmaLaunch;
 
 // Launch one fused kernel (N = 2^logn <= 4096) over a.batch rows.
 using FusedLaunchFn = cudaError_t (*)(const FusedArgs &a, bool dif, bool interleaved, cudaStream_t st);
 // Launch one pass group (2^L-point sub-problems) over a.batch rows.
 using PassLaunchFn = cudaError_t (*)(const PassArgs &a, bool dif, bool il_in, bool il_out,
                                      int64_t grid, cudaStream_t st);
+
+// Launch the persistent TMA-fed fused kernel (planar, 16-byte aligned rows).
+using TmaLaunchFn = cudaError_t (*)(const TmaLaunch &L, cudaStream_t st);
 
 constexpr int kFusedMaxLog = 12;
 constexpr int kMaxRadixLog = 5;
@@ -30,6 +34,11 @@ int pass_tile(int dtype);           // TJ: sub-problems per CTA
 int pass_default_lr(int dtype);
 PassLaunchFn pass_launcher_f32(int L);
 PassLaunchFn pass_launcher_f64(int L);
+
+TmaLaunchFn tma_launcher(int dtype, int logn, int lr, bool dif);
+TmaLaunchFn tma_launcher_f32(int logn, int lr, bool dif);
+TmaLaunchFn tma_launcher_f64(int logn, int lr, bool dif);
+int tma_default_lr(int dtype, int logn);   // -1: no TMA config for this size
 
 void count_launch();
 

@@ -1,0 +1,366 @@
+// sfft_tma.cuh -- persistent TMA-fed fused kernel for planar rows, N <= 4096.
+//
+// Same arithmetic and Stockham register passes as sfft_fused.cuh (the
+// reference's radix-2 stages, transform.py:208-270), but the global side is
+// moved by the Tensor Memory Accelerator instead of per-thread LDG/STG:
+//   * a tile = S consecutive signals of one plane is a 3-D TMA box
+//     (W elements per 128-byte line, N/W lines per signal, S signals) landing
+//     in shared memory with the 128-byte swizzle (16-byte chunk index XOR
+//     line index mod 8), STAGES tiles in flight per CTA (mbarrier
+//     complete_tx), so HBM reads never occupy the LSU/L1 wavefront pipe;
+//   * the first register pass reads the swizzled tile, intermediate passes
+//     exchange through a padded buffer (phys = e + e/R), the last pass writes
+//     a swizzled output tile that one thread stores with a TMA bulk tensor
+//     store (bulk_group, double-buffered);
+//   * CTAs are persistent (grid = resident CTAs, tiles round-robin).
+// Rows beyond the batch are zero-filled by the TMA load and clipped by the
+// TMA store, so the tail tile needs no predication.
+#pragma once
+#include <cuda.h>
+
+#include "sfft_common.cuh"
+
+namespace sfft {
+
+struct TmaArgs {
+    int64_t ntiles;
+    double scale;        // 1/N when the caller swapped the maps for the inverse
+    int scale_out;
+    const void *tw;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_LOOP:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra WAIT_DONE;\n"
+        "bra WAIT_LOOP;\n"
+        "WAIT_DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::
+            "r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, const void *src, int c0, int c1, int c2)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void bulk_wait_read()
+{
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// Shape of the TMA kernel.  NT_REQ: requested threads per CTA (>= P).
+template <typename T, int LOGN, int LR_REQ, int NT_REQ, int STAGES, int OB>
+struct TmaShape {
+    static constexpr int N = 1 << LOGN;
+    static constexpr int LR = cmin(LR_REQ, LOGN);
+    static constexpr int R = 1 << LR;
+    static constexpr int P = N / R;
+    static constexpr int NT = P > NT_REQ ? P : NT_REQ;
+    static constexpr int S = NT / P;                          // signals per tile
+    static constexpr int NPASS = (LOGN + LR - 1) / LR;
+    static constexpr int W = 128 / (int)sizeof(T);            // elements per 128-byte line
+    static constexpr int TILE = S * N * (int)sizeof(T);       // bytes per plane per tile
+    static constexpr int SSTR = N + (N >> LR);                // padded exchange stride
+    static constexpr int EXB = NPASS >= 2 ? 2 * S * SSTR * (int)sizeof(T) : 0;
+    static constexpr int IN_OFF = 0;
+    static constexpr int OUT_OFF = IN_OFF + STAGES * 2 * TILE;
+    static constexpr int EX_OFF = OUT_OFF + OB * 2 * TILE;
+    static constexpr int BAR_OFF = (EX_OFF + EXB + 15) / 16 * 16;
+    static constexpr int SMEM = BAR_OFF + STAGES * 8 + 1024;   // + alignment slack
+    static_assert(N >= W, "TMA path needs rows of at least one 128-byte line");
+    static_assert(N / W <= 256 && S <= 256, "TMA box dims are limited to 256");
+    static_assert(TILE % 1024 == 0, "swizzled tiles must stay 1024-byte aligned");
+};
+
+// byte offset of logical element e of local signal s inside a swizzled tile
+template <typename T, int N>
+__device__ __forceinline__ uint32_t swz(int s, int e)
+{
+    const uint32_t L = (uint32_t)(s * N + e) * (uint32_t)sizeof(T);
+    return L ^ ((L >> 3) & 0x70u);
+}
+
+template <typename T>
+__device__ __forceinline__ T lds_at(const unsigned char *base, uint32_t off)
+{
+    return *reinterpret_cast<const T *>(base + off);
+}
+
+template <typename T>
+__device__ __forceinline__ void sts_at(unsigned char *base, uint32_t off, T v)
+{
+    *reinterpret_cast<T *>(base + off) = v;
+}
+
+template <typename T, int LOGN, int LR_REQ, bool DIF, int NT_REQ, int STAGES, int OB>
+__global__ void __launch_bounds__(TmaShape<T, LOGN, LR_REQ, NT_REQ, STAGES, OB>::NT)
+sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant__ CUtensorMap in_im,
+                const __grid_constant__ CUtensorMap out_re, const __grid_constant__ CUtensorMap out_im,
+                const TmaArgs a)
+{
+    using Sh = TmaShape<T, LOGN, LR_REQ, NT_REQ, STAGES, OB>;
+    constexpr int N = Sh::N, R = Sh::R, P = Sh::P, S = Sh::S, LR = Sh::LR, NPASS = Sh::NPASS,
+                  TILE = Sh::TILE, SSTR = Sh::SSTR, W = Sh::W;
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char *smem = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *in_buf = smem + Sh::IN_OFF;      // [STAGES][2 planes][TILE]
+    unsigned char *out_buf = smem + Sh::OUT_OFF;    // [OB][2][TILE]
+    T *ex = reinterpret_cast<T *>(smem + Sh::EX_OFF);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + Sh::BAR_OFF);
+
+    const int tid = threadIdx.x;
+    const int sl = tid / P, t = tid % P;
+    const int64_t nk = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const TwDirect<T> tw{reinterpret_cast<const vec2_t<T> *>(a.tw), LOGN};
+    const T scale = (T)a.scale;
+    const bool do_scale = a.scale_out != 0;
+
+    auto issue_load = [&](int st, int64_t tile) {
+        uint64_t *bar = full + st;
+        mbar_expect_tx(bar, 2 * TILE);
+        const int row0 = (int)(tile * S);
+        tma_load_3d(in_buf + (st * 2 + 0) * TILE, &in_re, bar, 0, 0, row0);
+        tma_load_3d(in_buf + (st * 2 + 1) * TILE, &in_im, bar, 0, 0, row0);
+    };
+
+    if (tid == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&in_re)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&in_im)) : "memory");
+        for (int s = 0; s < STAGES; ++s) mbar_init(full + s, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int s = 0; s < STAGES && s < nk; ++s) issue_load(s, blockIdx.x + (int64_t)s * gridDim.x);
+    }
+
+    T vr[R], vi[R];
+    T *exr = ex + sl * SSTR;
+    T *exi = ex + S * SSTR + sl * SSTR;
+
+    for (int64_t k = 0; k < nk; ++k) {
+        const int st = (int)(k % STAGES);
+        const int ob = (int)(k % OB);
+        const int64_t tile = blockIdx.x + k * gridDim.x;
+        const unsigned char *inr = in_buf + (st * 2 + 0) * TILE;
+        const unsigned char *ini = in_buf + (st * 2 + 1) * TILE;
+        unsigned char *outr = out_buf + (ob * 2 + 0) * TILE;
+        unsigned char *outi = out_buf + (ob * 2 + 1) * TILE;
+        mbar_wait(full + st, (uint32_t)((k / STAGES) & 1));
+
+        if constexpr (!DIF) {
+            // ---------------- DIT ----------------
+#pragma unroll
+            for (int p = 0; p < NPASS; ++p) {
+                const int sp = p * LR;
+                const int kp = cmin(LR, LOGN - sp);
+#define SFFT_TMA_DIT(KP)                                                                              \
+    if constexpr (KP <= LR) if (kp == KP) {                                                          \
+        constexpr int RP = 1 << KP, U = R / RP;                                                      \
+        const int ns = 1 << sp;                                                                      \
+        _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
+        {                                                                                            \
+            const int j = t + P * u;                                                                 \
+            _Pragma("unroll") for (int r = 0; r < RP; ++r)                                           \
+            {                                                                                        \
+                const int e = j + r * (N / RP);                                                      \
+                if (p == 0) {                                                                        \
+                    vr[u * RP + r] = lds_at<T>(inr, swz<T, N>(sl, e));                               \
+                    vi[u * RP + r] = lds_at<T>(ini, swz<T, N>(sl, e));                               \
+                } else {                                                                             \
+                    vr[u * RP + r] = exr[e + (e >> LR)];                                             \
+                    vi[u * RP + r] = exi[e + (e >> LR)];                                             \
+                }                                                                                    \
+            }                                                                                        \
+        }                                                                                            \
+        _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
+        {                                                                                            \
+            const int j = t + P * u;                                                                 \
+            dit_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (int64_t)(j & (ns - 1)), tw);            \
+        }                                                                                            \
+        if (p < NPASS - 1) {                                                                         \
+            if (p > 0) __syncthreads();                                                              \
+            _Pragma("unroll") for (int u = 0; u < U; ++u)                                            \
+            {                                                                                        \
+                const int j = t + P * u;                                                             \
+                const int base = (j >> sp) * ns * RP + (j & (ns - 1));                               \
+                _Pragma("unroll") for (int f = 0; f < RP; ++f)                                       \
+                {                                                                                    \
+                    const int e = base + ns * f;                                                     \
+                    exr[e + (e >> LR)] = vr[u * RP + brev(f, KP)];                                   \
+                    exi[e + (e >> LR)] = vi[u * RP + brev(f, KP)];                                   \
+                }                                                                                    \
+            }                                                                                        \
+            if (p == 0) {                                                                            \
+                /* input stage consumed; output buffer `ob` must be free before B1 */              \
+                if (tid == 0) bulk_wait_read<OB - 1>();                                             \
+                __syncthreads();                                                                     \
+                if (tid == 0 && k + STAGES < nk) issue_load(st, tile + (int64_t)STAGES * gridDim.x); \
+            } else {                                                                                 \
+                __syncthreads();                                                                     \
+            }                                                                                        \
+        } else {                                                                                     \
+            if (NPASS == 1) {                                                                        \
+                if (tid == 0) bulk_wait_read<OB - 1>();                                             \
+                __syncthreads();                                                                     \
+                if (tid == 0 && k + STAGES < nk) issue_load(st, tile + (int64_t)STAGES * gridDim.x); \
+            }                                                                                        \
+            _Pragma("unroll") for (int u = 0; u < U; ++u)                                            \
+            {                                                                                        \
+                const int j = t + P * u;                                                             \
+                _Pragma("unroll") for (int f = 0; f < RP; ++f)                                       \
+                {                                                                                    \
+                    const int e = j + ns * f;                                                        \
+                    T re = vr[u * RP + brev(f, KP)], im = vi[u * RP + brev(f, KP)];                  \
+                    if (do_scale) { re *= scale; im *= scale; }                                      \
+                    sts_at<T>(outr, swz<T, N>(sl, e), re);                                           \
+                    sts_at<T>(outi, swz<T, N>(sl, e), im);                                           \
+                }                                                                                    \
+            }                                                                                        \
+        }                                                                                            \
+    }
+                SFFT_TMA_DIT(1)
+                SFFT_TMA_DIT(2)
+                SFFT_TMA_DIT(3)
+                SFFT_TMA_DIT(4)
+                SFFT_TMA_DIT(5)
+#undef SFFT_TMA_DIT
+            }
+        } else {
+            // ---------------- DIF (transpose) ----------------
+#pragma unroll
+            for (int q = 0; q < NPASS; ++q) {
+                const int p = NPASS - 1 - q;
+                const int sp = p * LR;
+                const int kp = cmin(LR, LOGN - sp);
+#define SFFT_TMA_DIF(KP)                                                                              \
+    if constexpr (KP <= LR) if (kp == KP) {                                                          \
+        constexpr int RP = 1 << KP, U = R / RP;                                                      \
+        const int ns = 1 << sp;                                                                      \
+        _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
+        {                                                                                            \
+            const int j = t + P * u;                                                                 \
+            const int base = (j >> sp) * ns * RP + (j & (ns - 1));                                   \
+            _Pragma("unroll") for (int f = 0; f < RP; ++f)                                           \
+            {                                                                                        \
+                const int e = base + ns * f;                                                         \
+                const int d = u * RP + brev(f, KP);                                                  \
+                if (q == 0) {                                                                        \
+                    vr[d] = lds_at<T>(inr, swz<T, N>(sl, e));                                        \
+                    vi[d] = lds_at<T>(ini, swz<T, N>(sl, e));                                        \
+                } else {                                                                             \
+                    vr[d] = exr[e + (e >> LR)];                                                      \
+                    vi[d] = exi[e + (e >> LR)];                                                      \
+                }                                                                                    \
+            }                                                                                        \
+        }                                                                                            \
+        _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
+        {                                                                                            \
+            const int j = t + P * u;                                                                 \
+            dif_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (int64_t)(j & (ns - 1)), tw);            \
+        }                                                                                            \
+        if (p > 0) {                                                                                 \
+            if (q > 0) __syncthreads();                                                              \
+            _Pragma("unroll") for (int u = 0; u < U; ++u)                                            \
+            {                                                                                        \
+                const int j = t + P * u;                                                             \
+                _Pragma("unroll") for (int r = 0; r < RP; ++r)                                       \
+                {                                                                                    \
+                    const int e = j + r * (N / RP);                                                  \
+                    exr[e + (e >> LR)] = vr[u * RP + r];                                             \
+                    exi[e + (e >> LR)] = vi[u * RP + r];                                             \
+                }                                                                                    \
+            }                                                                                        \
+            if (q == 0) {                                                                            \
+                if (tid == 0) bulk_wait_read<OB - 1>();                                             \
+                __syncthreads();                                                                     \
+                if (tid == 0 && k + STAGES < nk) issue_load(st, tile + (int64_t)STAGES * gridDim.x); \
+            } else {                                                                                 \
+                __syncthreads();                                                                     \
+            }                                                                                        \
+        } else {                                                                                     \
+            if (NPASS == 1) {                                                                        \
+                if (tid == 0) bulk_wait_read<OB - 1>();                                             \
+                __syncthreads();                                                                     \
+                if (tid == 0 && k + STAGES < nk) issue_load(st, tile + (int64_t)STAGES * gridDim.x); \
+            }                                                                                        \
+            _Pragma("unroll") for (int u = 0; u < U; ++u)                                            \
+            {                                                                                        \
+                const int j = t + P * u;                                                             \
+                _Pragma("unroll") for (int r = 0; r < RP; ++r)                                       \
+                {                                                                                    \
+                    const int e = j + r * (N / RP);                                                  \
+                    T re = vr[u * RP + r], im = vi[u * RP + r];                                      \
+                    if (do_scale) { re *= scale; im *= scale; }                                      \
+                    sts_at<T>(outr, swz<T, N>(sl, e), re);                                           \
+                    sts_at<T>(outi, swz<T, N>(sl, e), im);                                           \
+                }                                                                                    \
+            }                                                                                        \
+        }                                                                                            \
+    }
+                SFFT_TMA_DIF(1)
+                SFFT_TMA_DIF(2)
+                SFFT_TMA_DIF(3)
+                SFFT_TMA_DIF(4)
+                SFFT_TMA_DIF(5)
+#undef SFFT_TMA_DIF
+            }
+        }
+        // output tile complete in shared memory -> one TMA store per plane
+        fence_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            const int row0 = (int)(tile * S);
+            tma_store_3d(&out_re, outr, 0, 0, row0);
+            tma_store_3d(&out_im, outi, 0, 0, row0);
+            bulk_commit();
+        }
+    }
+    if (tid == 0) bulk_wait_all();
+    (void)W;
+}
+
+}  // namespace sfft

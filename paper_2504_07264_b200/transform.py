@@ -82,14 +82,15 @@ class FftPlan:
 
     def __repr__(self):
         return (f"FftPlan(m={self.m}, algorithm={self.algorithm}, dtype={self.dtype}, "
-                f"device={self.device}, radix=2^{self.radix_log}, launches={self.launches_per_exec})")
+                f"device={self.device}, kernel={self.kernel}, radix=2^{self.radix_log}, "
+                f"launches={self.launches_per_exec})")
 
     @property
     def sample_count(self) -> int:
         return 1 << self.m
 
     def _info(self):
-        vals = [ctypes.c_int() for _ in range(6)]
+        vals = [ctypes.c_int() for _ in range(7)]
         _ffi.check(_ffi.lib.sfft_plan_info(self._handle, *[ctypes.byref(v) for v in vals]))
         return [v.value for v in vals]
 
@@ -100,6 +101,12 @@ class FftPlan:
     @property
     def radix_log(self) -> int:
         return self._info()[5]
+
+    @property
+    def kernel(self) -> str:
+        """Kernel family used for aligned planar rows: 'tma', 'ldg' or 'pass'."""
+        return {_ffi.SFFT_KERNEL_TMA: "tma", _ffi.SFFT_KERNEL_LDG: "ldg",
+                _ffi.SFFT_KERNEL_PASS: "pass"}[self._info()[6]]
 
     def workspace_bytes(self, batch: int) -> int:
         out = ctypes.c_size_t()
@@ -135,13 +142,15 @@ class FftPlan:
 
 
 def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
-              dtype=torch.float64, device=None, radix_log: int = 0) -> FftPlan:
+              dtype=torch.float64, device=None, radix_log: int = 0, kernel: str = "auto") -> FftPlan:
     """Build an FftPlan for 2**m samples on a CUDA device (transform.py:65-85).
 
     Same validation order and messages as the reference: m < 0 -> ValueError,
     m > max_m -> CapacityError, unknown algorithm -> ValueError.  ``dtype`` is
     the plane dtype (float64 like the reference, or float32); ``radix_log``
-    overrides the register radix of the fused kernel (0 = tuned default).
+    overrides the register radix of the fused kernel (0 = tuned default);
+    ``kernel`` picks the fused kernel family: "auto" (TMA-fed when the rows
+    allow it), "ldg" (per-thread loads) or "tma" (required).
     """
     if m < 0:
         raise ValueError(f"stage count m must be >= 0, got {m}")
@@ -151,11 +160,14 @@ def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
     if dtype not in _DTYPE_CODE:
         raise ValueError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
     device = _resolve_device(device)
+    kernels = {"auto": _ffi.SFFT_KERNEL_AUTO, "ldg": _ffi.SFFT_KERNEL_LDG, "tma": _ffi.SFFT_KERNEL_TMA}
+    if kernel not in kernels:
+        raise ValueError(f"kernel must be one of {sorted(kernels)}, got {kernel!r}")
     handle = ctypes.c_void_p()
     algo = _ffi.SFFT_DIF if algorithm is Algorithm.DIF else _ffi.SFFT_DIT
     _ffi.check(_ffi.lib.sfft_plan_create_ex(int(m), _DTYPE_CODE[dtype], algo, device.index,
                                             int(min(max_m, MAX_PLAN_M)),
-                                            int(radix_log), ctypes.byref(handle)))
+                                            int(radix_log), kernels[kernel], ctypes.byref(handle)))
     return FftPlan(m, algorithm, dtype, device, handle.value)
 
 

@@ -184,3 +184,54 @@ def test_launches_are_counted(cuda):
     sf.fft_split(x, x)
     torch.cuda.synchronize()
     assert _ffi.launch_count() == before + 1
+
+
+# ---- the TMA-fed persistent kernel vs the LDG kernel vs the oracle -----------
+
+TMA_CASES = [("f32", m, lr) for m, lrs in {5: [3], 6: [3, 2], 7: [3, 4], 8: [3, 4], 9: [3, 4],
+                                            10: [4, 3, 5], 11: [4, 3], 12: [4, 3]}.items() for lr in lrs] + \
+            [("f64", m, lr) for m, lrs in {4: [2], 5: [3], 6: [3], 7: [3, 4], 8: [3, 4], 9: [3],
+                                            10: [3, 4], 11: [4]}.items() for lr in lrs]
+
+
+@pytest.mark.parametrize("algo", ["dit", "dif"])
+@pytest.mark.parametrize("dt,m,lr", TMA_CASES)
+def test_tma_kernel_many_tiles(cuda, dt, m, lr, algo):
+    # enough rows for several tiles per persistent CTA (stage and output-buffer
+    # reuse) plus a ragged tail tile
+    dtype = np.float32 if dt == "f32" else np.float64
+    tdt = torch.float32 if dt == "f32" else torch.float64
+    b = (1 << 22 >> m) + 3
+    rng = np.random.default_rng(7000 + m + 31 * lr)
+    re, im = rand(rng, b, 1 << m, dtype)
+    plan = sf.make_plan(m, algo, dtype=tdt, device="cuda:0", radix_log=lr, kernel="tma")
+    assert plan.kernel == "tma"
+    xr, xi = torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda()
+    for inverse in (False, True):
+        yr, yi = sf.fft_split(xr, xi, plan=plan, inverse=inverse)
+        gr, gi = yr.cpu().numpy(), yi.cpu().numpy()
+        wr, wi = oracle.fft_split_c(re, im, algo, inverse)
+        if dt == "f64":
+            assert np.array_equal(bits(gr), bits(wr)) and np.array_equal(bits(gi), bits(wi))
+        else:
+            assert rel_l2(gr.astype(np.float64), gi.astype(np.float64), wr, wi) <= F32_TOL(m)
+            # and bit-identical to the LDG kernel (same arithmetic, other data path)
+            ldg = sf.make_plan(m, algo, dtype=tdt, device="cuda:0", radix_log=lr, kernel="ldg")
+            lr_, li_ = sf.fft_split(xr, xi, plan=ldg, inverse=inverse)
+            assert torch.equal(lr_, yr) and torch.equal(li_, yi)
+
+
+def test_tma_falls_back_for_unaligned_rows(cuda):
+    m = 6
+    rng = np.random.default_rng(8)
+    base_r = torch.from_numpy(rng.standard_normal(64 * 100 + 1).astype(np.float32)).cuda()
+    base_i = torch.from_numpy(rng.standard_normal(64 * 100 + 1).astype(np.float32)).cuda()
+    xr, xi = base_r[1:].view(100, 64), base_i[1:].view(100, 64)     # 4-byte aligned only
+    plan = sf.make_plan(m, dtype=torch.float32, device="cuda:0")
+    assert plan.kernel == "tma"
+    yr, yi = sf.fft_split(xr, xi, plan=plan)                         # auto -> LDG path
+    wr, wi = oracle.fft_split_c(xr.cpu().numpy(), xi.cpu().numpy())
+    assert rel_l2(yr.cpu().numpy().astype(np.float64), yi.cpu().numpy().astype(np.float64), wr, wi) <= 6e-5
+    forced = sf.make_plan(m, dtype=torch.float32, device="cuda:0", kernel="tma")
+    with pytest.raises(ValueError, match="TMA kernel needs"):
+        sf.fft_split(xr, xi, plan=forced)
