@@ -132,8 +132,9 @@ struct sfft_plan {
     int lr_tma = -1;                // radix of the TMA kernel (-1: none)
     int lr_ldg_il = 0;              // radix of the interleaved LDG kernel
     // fused path
-    void *d_tw = nullptr;          // vec2_t<T> table of stage tw_top
-    int tw_top = 0;
+    void *d_tw = nullptr;          // stage-major vec2_t<T> table, stages 1..cat_top
+    int cat_top = 0;
+    void *d_top = nullptr;         // fp64 m > 20: stage-m table for stages > cat_top
     // large path
     double2 *d_coarse = nullptr;
     int coarse_log = 0;
@@ -144,22 +145,45 @@ struct sfft_plan {
 namespace {
 
 template <typename T>
-int upload_table(sfft_plan *p, int top)
+int upload_table(sfft_plan *p, int cat_top, bool with_top)
 {
-    // stage `top` factors, 2^(top-1) entries, in the plan dtype
-    const int64_t h = top >= 1 ? int64_t(1) << (top - 1) : 1;
-    std::vector<double> wr((size_t)h, 1.0), wi((size_t)h, 0.0);
-    if (top >= 1) stage_table(top, h, wr.data(), wi.data());
-    std::vector<vec2_t<T>> host((size_t)h);
-    for (int64_t q = 0; q < h; ++q) {
-        host[q].x = (T)wr[q];
-        host[q].y = (T)wi[q];
+    // stage-major: stage i (1..cat_top) at offset 2^(i-1)-1, bitwise the
+    // strided view [::2^(cat_top-i)] of the stage-cat_top table
+    const int64_t total = cat_top >= 1 ? (int64_t(1) << cat_top) - 1 : 1;
+    std::vector<vec2_t<T>> host((size_t)total);
+    if (cat_top >= 1) {
+        const int64_t h = int64_t(1) << (cat_top - 1);
+        std::vector<double> wr((size_t)h), wi((size_t)h);
+        stage_table(cat_top, h, wr.data(), wi.data());
+        for (int i = 1; i <= cat_top; ++i) {
+            const int64_t off = (int64_t(1) << (i - 1)) - 1, sh = cat_top - i;
+            for (int64_t q = 0; q < (int64_t(1) << (i - 1)); ++q) {
+                host[off + q].x = (T)wr[q << sh];
+                host[off + q].y = (T)wi[q << sh];
+            }
+        }
+    } else {
+        host[0].x = (T)1;
+        host[0].y = (T)0;
     }
-    cudaError_t e = cudaMalloc(&p->d_tw, sizeof(vec2_t<T>) * (size_t)h);
+    cudaError_t e = cudaMalloc(&p->d_tw, sizeof(vec2_t<T>) * (size_t)total);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(twiddle table)");
-    e = cudaMemcpy(p->d_tw, host.data(), sizeof(vec2_t<T>) * (size_t)h, cudaMemcpyHostToDevice);
+    e = cudaMemcpy(p->d_tw, host.data(), sizeof(vec2_t<T>) * (size_t)total, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(twiddle table)");
-    p->tw_top = top;
+    p->cat_top = cat_top;
+    if (with_top) {
+        const int64_t h = int64_t(1) << (p->log2n - 1);
+        std::vector<double> wr((size_t)h), wi((size_t)h);
+        stage_table(p->log2n, h, wr.data(), wi.data());
+        std::vector<vec2_t<T>> top((size_t)h);
+        for (int64_t q = 0; q < h; ++q) {
+            top[q].x = (T)wr[q];
+            top[q].y = (T)wi[q];
+        }
+        e = cudaMalloc(&p->d_top, sizeof(vec2_t<T>) * (size_t)h);
+        if (e == cudaSuccess) e = cudaMemcpy(p->d_top, top.data(), sizeof(vec2_t<T>) * (size_t)h, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "uploading the stage-m table");
+    }
     return SFFT_OK;
 }
 
@@ -191,6 +215,7 @@ void free_plan(sfft_plan *p)
 {
     if (!p) return;
     if (p->d_tw) cudaFree(p->d_tw);
+    if (p->d_top) cudaFree(p->d_top);
     if (p->d_coarse) cudaFree(p->d_coarse);
     if (p->d_fine) cudaFree(p->d_fine);
     delete p;
@@ -328,7 +353,8 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         a.swap_out = last && inv;
         a.scale = last ? scale : 1.0;
         a.tw = p->d_tw;
-        a.tw_top = p->tw_top;
+        a.tw_cat_top = p->cat_top;
+        a.tw_top_tab = p->d_top;
         a.coarse = p->d_coarse;
         a.coarse_log = p->coarse_log;
         a.fine = p->d_fine;
@@ -407,31 +433,38 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
     int rc = SFFT_OK;
     p->kernel = kernel;
     if (log2n <= kFusedMaxLog) {
-        const int tma_lr = tma_default_lr(dtype, log2n);
-        int lr = log2_radix > 0 ? log2_radix
-                                : (kernel != SFFT_KERNEL_LDG && tma_lr >= 0 ? tma_lr : fused_default_lr(dtype, log2n));
+        bool auto_tma = false;
+        int auto_lr = 0;
+        auto_choice(dtype, log2n, &auto_tma, &auto_lr);
+        int lr;
+        if (log2_radix > 0) lr = log2_radix;
+        else if (kernel == SFFT_KERNEL_AUTO) lr = auto_lr;
+        else if (kernel == SFFT_KERNEL_TMA) lr = tma_default_lr(dtype, log2n);
+        else lr = fused_default_lr(dtype, log2n);
         if (log2n == 0) lr = 0;
         if (lr > log2n) lr = log2n;
-        if (!fused_launcher_algo(dtype, log2n, lr, algorithm == SFFT_DIF, false)) {
+        if (lr < 0 || !fused_launcher_algo(dtype, log2n, lr, algorithm == SFFT_DIF, false)) {
             delete p;
             return fail(SFFT_EINVAL, "radix 2^%d is not available for log2n=%d", lr, log2n);
         }
         p->lr = lr;
         p->lr_ldg_il = fused_default_lr(dtype, log2n);
-        if (kernel != SFFT_KERNEL_LDG && tma_launcher(dtype, log2n, lr, false)) p->lr_tma = lr;
+        const bool want_tma = kernel == SFFT_KERNEL_TMA ||
+                              (kernel == SFFT_KERNEL_AUTO && (log2_radix > 0 || auto_tma));
+        if (want_tma && tma_launcher(dtype, log2n, lr, false)) p->lr_tma = lr;
         if (kernel == SFFT_KERNEL_TMA && p->lr_tma < 0) {
             delete p;
             return fail(SFFT_EINVAL, "no TMA kernel for log2n=%d radix=2^%d", log2n, lr);
         }
-        rc = dtype == SFFT_F32 ? upload_table<float>(p, log2n) : upload_table<double>(p, log2n);
+        rc = dtype == SFFT_F32 ? upload_table<float>(p, log2n, false) : upload_table<double>(p, log2n, false);
     } else {
         p->lr = pass_default_lr(dtype);
         p->groups = split_groups(log2n);
         if (dtype == SFFT_F32) {
-            rc = upload_table<float>(p, kFusedMaxLog);
+            rc = upload_table<float>(p, kFusedMaxLog, false);
             if (rc == SFFT_OK) rc = upload_two_level(p);
         } else {
-            rc = upload_table<double>(p, log2n);
+            rc = upload_table<double>(p, log2n < 20 ? log2n : 20, log2n > 20);
         }
     }
     if (rc != SFFT_OK) {

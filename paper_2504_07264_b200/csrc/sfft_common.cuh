@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "sfft_layouts.h"
+
 namespace sfft {
 
 template <typename T> struct Vec2;
@@ -62,33 +64,52 @@ __device__ __forceinline__ void st_stream(double *p, double v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(float2 *p, float2 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }
 
-// Twiddle source for the stages of one launch.
-//   Direct: stage i, index q -> tab[q << (top - i)] where tab is the
-//           stage-`top` factor table (every stage table is a bitwise strided
-//           view of it).
-//   TwoLevel (fp32, stages above the coarse table, large N only): the
-//           factor is coarse[hi] * fine[lo] evaluated in fp64 and rounded.
+// Twiddle sources.  All stage tables are bitwise strided views of the top one
+// (SURVEY.md sec. 3B), but the kernels read them "stage-major": stage i's
+// 2^(i-1) factors stored contiguously at offset 2^(i-1)-1, so that the lanes
+// of a warp (consecutive q) read consecutive 8/16-byte entries instead of one
+// cache line each.
+//   TwCat:      stages 1..m from the stage-major table (m <= 20).
+//   TwCatTop:   stage-major up to cat_top, then the stage-m table read with
+//               stride 2^(m-i) (fp64 plans with m > 20 only).
+//   TwTwoLevel: fp32 N > 4096: stage-major fp32 table up to cat_top (12);
+//               above it coarse[hi] * fine[lo] in fp64, rounded to fp32.
 template <typename T>
-struct TwDirect {
+struct TwCat {
+    using index_t = int;
     const vec2_t<T> *tab;
+    __device__ __forceinline__ vec2_t<T> get(int i, int q) const
+    {
+        return ldtw(tab + ((1 << (i - 1)) - 1) + q);
+    }
+};
+
+template <typename T>
+struct TwCatTop {
+    using index_t = int64_t;
+    const vec2_t<T> *tab;      // stage-major, stages 1..cat_top
+    int cat_top;
+    const vec2_t<T> *top_tab;  // stage `top` table (2^(top-1) entries)
     int top;
     __device__ __forceinline__ vec2_t<T> get(int i, int64_t q) const
     {
-        return ldtw(tab + (q << (top - i)));
+        if (i <= cat_top) return ldtw(tab + ((int64_t(1) << (i - 1)) - 1) + q);
+        return ldtw(top_tab + (q << (top - i)));
     }
 };
 
 template <typename T>
 struct TwTwoLevel {
-    const vec2_t<T> *tab;      // direct table of stage `top` (top <= coarse_log)
-    int top;
+    using index_t = int64_t;
+    const vec2_t<T> *tab;      // stage-major fp32, stages 1..cat_top
+    int cat_top;
     const double2 *coarse;     // stage coarse_log factors, 2^(coarse_log-1) entries
     int coarse_log;
     const double2 *fine;       // exp(-j 2 pi lo / 2^m), lo < 2^(m - coarse_log)
     int m;
     __device__ __forceinline__ vec2_t<T> get(int i, int64_t q) const
     {
-        if (i <= top) return ldtw(tab + (q << (top - i)));
+        if (i <= cat_top) return ldtw(tab + ((int64_t(1) << (i - 1)) - 1) + q);
         const int64_t qq = q << (m - i);
         const int fb = m - coarse_log;
         const double2 a = __ldg(coarse + (qq >> fb));
@@ -102,6 +123,32 @@ struct TwTwoLevel {
     }
 };
 
+// Physical slot of logical element e in shared-memory exchange x (the buffer
+// between register pass x and x+1, DIT numbering), per the planned layout
+// (sfft_layouts.h, tools/plan_layouts.py).
+template <typename T, int LOGN, int LR, int NT>
+__device__ __forceinline__ int ex_phys(int x, int e)
+{
+    using L = ExLayout<(int)sizeof(T), LOGN, LR, NT>;
+    constexpr int mask = sizeof(T) == 4 ? 31 : 15;
+    const int kind = L::kind(x), a = L::arg(x);
+    return kind == 0 ? e : kind == 1 ? e + (e >> a) : (e ^ ((e >> a) & mask));
+}
+
+template <typename T, int LOGN, int LR, int NT>
+__host__ __device__ constexpr int ex_sstr()
+{
+    return ExLayout<(int)sizeof(T), LOGN, LR, NT>::sstr;
+}
+
+// fp32 skips the identity and quarter-turn factors of the first stages
+// (count_flops' census: identity rotations cost nothing, a quarter turn is a
+// swap/negate, transform.py:312-321).  fp64 multiplies by every factor
+// exactly as the reference executor does (transform.py:131-150), which keeps
+// it bit-identical including signed zeros.
+template <typename T> struct SkipTrivial { static constexpr bool value = false; };
+template <> struct SkipTrivial<float> { static constexpr bool value = true; };
+
 // K consecutive DIT stages (global stages gs+1 .. gs+K) on the 2^K values
 // v[0..2^K) of one virtual thread.  Register position p holds, before stage
 // t, the (size 2^(gs+t-1)) partial transform of sub-sequence (p mod
@@ -111,8 +158,9 @@ struct TwTwoLevel {
 // reference by tests/test_schedule_model.py (a numpy restatement of exactly
 // this index map).
 template <typename T, int K, typename TW>
-__device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, int64_t cbase, const TW &tw)
+__device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw)
 {
+    using I = typename TW::index_t;
 #pragma unroll
     for (int t = 1; t <= K; ++t) {
         const int half = (1 << K) >> t;
@@ -120,14 +168,21 @@ __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, int64_t cbase, 
 #pragma unroll
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;
+            // 0: stage 1 (no factor), 1: identity, 2: quarter turn, 3: generic
+            const int kind = i == 1 ? 0
+                           : (SkipTrivial<T>::value && gs == 0 && f == 0) ? 1
+                           : (SkipTrivial<T>::value && gs == 0 && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w;
-            if (i > 1) w = tw.get(i, cbase + ((int64_t)f << gs));
+            if (kind == 3) w = tw.get(i, cbase + ((I)f << gs));
 #pragma unroll
             for (int r = 0; r < half; ++r) {
                 const int p1 = r + rf, p2 = p1 + half;
                 T tr, ti;
-                if (i > 1) {
+                if (kind == 3) {
                     cmul(vr[p2], vi[p2], w.x, w.y, tr, ti);
+                } else if (kind == 2) {
+                    tr = vi[p2];
+                    ti = -vr[p2];
                 } else {
                     tr = vr[p2];
                     ti = vi[p2];
@@ -144,8 +199,9 @@ __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, int64_t cbase, 
 // Transpose of dit_stages: DIF stages gs+K .. gs+1 (descending), same
 // register map run backwards.
 template <typename T, int K, typename TW>
-__device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, int64_t cbase, const TW &tw)
+__device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw)
 {
+    using I = typename TW::index_t;
 #pragma unroll
     for (int t = K; t >= 1; --t) {
         const int half = (1 << K) >> t;
@@ -153,8 +209,11 @@ __device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, int64_t cbase, 
 #pragma unroll
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;
+            const int kind = i == 1 ? 0
+                           : (SkipTrivial<T>::value && gs == 0 && f == 0) ? 1
+                           : (SkipTrivial<T>::value && gs == 0 && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w;
-            if (i > 1) w = tw.get(i, cbase + ((int64_t)f << gs));
+            if (kind == 3) w = tw.get(i, cbase + ((I)f << gs));
 #pragma unroll
             for (int r = 0; r < half; ++r) {
                 const int p1 = r + rf, p2 = p1 + half;
@@ -162,8 +221,11 @@ __device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, int64_t cbase, 
                 const T ti = sub_rn(vi[p1], vi[p2]);
                 vr[p1] = add_rn(vr[p1], vr[p2]);
                 vi[p1] = add_rn(vi[p1], vi[p2]);
-                if (i > 1) {
+                if (kind == 3) {
                     cmul(tr, ti, w.x, w.y, vr[p2], vi[p2]);
+                } else if (kind == 2) {
+                    vr[p2] = ti;
+                    vi[p2] = -tr;
                 } else {
                     vr[p2] = tr;
                     vi[p2] = ti;

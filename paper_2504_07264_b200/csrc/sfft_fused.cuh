@@ -24,7 +24,7 @@ namespace sfft {
 struct FusedArgs {
     const void *x0, *x1;   // planar: re, im planes; interleaved: x0 = pairs
     void *y0, *y1;
-    const void *tw;        // vec2_t<T>[N/2] stage-LOGN factor table
+    const void *tw;        // stage-major factor table, stages 1..LOGN (N-1 entries)
     int64_t batch;
     int64_t in_stride, out_stride;   // elements (planar) or pairs (interleaved)
     int inverse;           // channel-swap inverse (transform.py:286-298)
@@ -104,13 +104,12 @@ struct FusedShape {
     static constexpr int NT = P > 256 ? P : 256;          // threads per block
     static constexpr int S = NT / P;                      // signals per block
     static constexpr int NPASS = LOGN == 0 ? 0 : (LOGN + LR - 1) / LR;
-    static constexpr int SSTR = N + (N >> LR);            // padded plane stride
     template <typename T>
-    static constexpr int smem_bytes() { return NPASS >= 2 ? 2 * S * SSTR * (int)sizeof(T) : 0; }
+    static constexpr int sstr() { return LOGN == 0 ? 1 : ex_sstr<T, LOGN, LR, NT>(); }   // per-signal plane stride
+    template <typename T>
+    static constexpr int smem_bytes() { return NPASS >= 2 ? 2 * S * sstr<T>() * (int)sizeof(T) : 0; }
 };
 
-template <int LR>
-__device__ __forceinline__ int sphys(int e) { return e + (e >> LR); }
 
 template <int P>
 __device__ __forceinline__ void sig_sync()
@@ -122,7 +121,7 @@ __device__ __forceinline__ void sig_sync()
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool valid,
                                          T *sr, T *si, const GIO<T, IL> &io,
-                                         const TwDirect<T> &tw)
+                                         const TwCat<T> &tw)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
     constexpr int N = Sh::N, R = Sh::R, P = Sh::P, LR = Sh::LR;
@@ -142,8 +141,8 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
                 if (valid) io.load(row, e, vr[u * RP + r], vi[u * RP + r]);
                 else { vr[u * RP + r] = T(0); vi[u * RP + r] = T(0); }
             } else {
-                vr[u * RP + r] = sr[sphys<LR>(e)];
-                vi[u * RP + r] = si[sphys<LR>(e)];
+                vr[u * RP + r] = sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
+                vi[u * RP + r] = si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
             }
         }
     }
@@ -151,7 +150,7 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = t + P * u;
-        dit_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (int64_t)(j & (NS - 1)), tw);
+        dit_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (j & (NS - 1)), tw);
     }
     // scatter in Stockham order
     if constexpr (!LAST) {
@@ -163,8 +162,8 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
 #pragma unroll
             for (int f = 0; f < RP; ++f) {
                 const int e = base + NS * f;
-                sr[sphys<LR>(e)] = vr[u * RP + brev(f, KP)];
-                si[sphys<LR>(e)] = vi[u * RP + brev(f, KP)];
+                sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = vr[u * RP + brev(f, KP)];
+                si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = vi[u * RP + brev(f, KP)];
             }
         }
         sig_sync<P>();
@@ -183,7 +182,7 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dit_from(T *vr, T *vi, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL> &io, const TwDirect<T> &tw)
+                                         T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw)
 {
     if constexpr (p < FusedShape<LOGN, LR_REQ>::NPASS) {
         dit_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw);
@@ -195,7 +194,7 @@ __device__ __forceinline__ void dit_from(T *vr, T *vi, int t, int64_t row, bool 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool valid,
                                          T *sr, T *si, const GIO<T, IL> &io,
-                                         const TwDirect<T> &tw)
+                                         const TwCat<T> &tw)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
     constexpr int N = Sh::N, R = Sh::R, P = Sh::P, LR = Sh::LR;
@@ -216,15 +215,15 @@ __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool 
                 if (valid) io.load(row, e, vr[d], vi[d]);
                 else { vr[d] = T(0); vi[d] = T(0); }
             } else {
-                vr[d] = sr[sphys<LR>(e)];
-                vi[d] = si[sphys<LR>(e)];
+                vr[d] = sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
+                vi[d] = si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
             }
         }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = t + P * u;
-        dif_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (int64_t)(j & (NS - 1)), tw);
+        dif_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (j & (NS - 1)), tw);
     }
     if constexpr (!LAST) {
         if constexpr (!FIRST) sig_sync<P>();
@@ -234,8 +233,8 @@ __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool 
 #pragma unroll
             for (int r = 0; r < RP; ++r) {
                 const int e = j + r * (N / RP);
-                sr[sphys<LR>(e)] = vr[u * RP + r];
-                si[sphys<LR>(e)] = vi[u * RP + r];
+                sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = vr[u * RP + r];
+                si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = vi[u * RP + r];
             }
         }
         sig_sync<P>();
@@ -254,7 +253,7 @@ __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool 
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dif_from(T *vr, T *vi, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL> &io, const TwDirect<T> &tw)
+                                         T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw)
 {
     if constexpr (p >= 0) {
         dif_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw);
@@ -267,7 +266,7 @@ __global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT)
 sfft_fused_kernel(const FusedArgs a)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
-    constexpr int R = Sh::R, P = Sh::P, S = Sh::S, SSTR = Sh::SSTR;
+    constexpr int R = Sh::R, P = Sh::P, S = Sh::S, SSTR = Sh::template sstr<T>();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *sbase = reinterpret_cast<T *>(smem_raw);
 
@@ -276,7 +275,7 @@ sfft_fused_kernel(const FusedArgs a)
     const int64_t row = (int64_t)blockIdx.x * S + sl;
     const bool valid = row < a.batch;
     const GIO<T, IL> io(a);
-    const TwDirect<T> tw{reinterpret_cast<const vec2_t<T> *>(a.tw), LOGN};
+    const TwCat<T> tw{reinterpret_cast<const vec2_t<T> *>(a.tw)};
 
     if constexpr (LOGN == 0) {
         if (valid) {

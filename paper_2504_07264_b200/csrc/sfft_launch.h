@@ -39,6 +39,7 @@ TmaLaunchFn tma_launcher(int dtype, int logn, int lr, bool dif);
 TmaLaunchFn tma_launcher_f32(int logn, int lr, bool dif);
 TmaLaunchFn tma_launcher_f64(int logn, int lr, bool dif);
 int tma_default_lr(int dtype, int logn);   // -1: no TMA config for this size
+void auto_choice(int dtype, int logn, bool *tma, int *lr);  // kernel=auto pick, 0 <= logn <= 12
 
 void count_launch();
 

@@ -31,8 +31,9 @@ struct PassArgs {
     int S;                 // stage offset of this group
     int swap_in, swap_out; // channel swap of the inverse (first / last launch)
     double scale;          // applied at the destination when swap_out
-    const void *tw;        // direct table of stage tw_top (vec2_t<T>)
-    int tw_top;
+    const void *tw;        // stage-major table, stages 1..tw_cat_top (vec2_t<T>)
+    int tw_cat_top;
+    const void *tw_top_tab;// fp64, m > 20: stage-m table for the stages above tw_cat_top
     const double2 *coarse; // two-level fp32 twiddles (see TwTwoLevel)
     int coarse_log;
     const double2 *fine;
@@ -106,7 +107,7 @@ __device__ __forceinline__ PIO<T, IL> make_pio(const PassArgs &a)
 }
 
 template <typename T, bool TWO>
-struct TwSel { using type = TwDirect<T>; };
+struct TwSel { using type = TwCatTop<T>; };
 template <typename T>
 struct TwSel<T, true> { using type = TwTwoLevel<T>; };
 
@@ -115,8 +116,11 @@ __device__ __forceinline__ typename TwSel<T, TWO>::type make_tw(const PassArgs &
 {
     typename TwSel<T, TWO>::type tw;
     tw.tab = (const vec2_t<T> *)a.tw;
-    tw.top = a.tw_top;
-    if constexpr (TWO) {
+    tw.cat_top = a.tw_cat_top;
+    if constexpr (!TWO) {
+        tw.top_tab = (const vec2_t<T> *)a.tw_top_tab;
+        tw.top = a.m;
+    } else {
         tw.coarse = a.coarse;
         tw.coarse_log = a.coarse_log;
         tw.fine = a.fine;

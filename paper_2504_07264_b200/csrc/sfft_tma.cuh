@@ -103,7 +103,7 @@ struct TmaShape {
     static constexpr int NPASS = (LOGN + LR - 1) / LR;
     static constexpr int W = 128 / (int)sizeof(T);            // elements per 128-byte line
     static constexpr int TILE = S * N * (int)sizeof(T);       // bytes per plane per tile
-    static constexpr int SSTR = N + (N >> LR);                // padded exchange stride
+    static constexpr int SSTR = ex_sstr<T, LOGN, LR, NT>();   // planned exchange stride
     static constexpr int EXB = NPASS >= 2 ? 2 * S * SSTR * (int)sizeof(T) : 0;
     static constexpr int IN_OFF = 0;
     static constexpr int OUT_OFF = IN_OFF + STAGES * 2 * TILE;
@@ -154,7 +154,7 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
     const int tid = threadIdx.x;
     const int sl = tid / P, t = tid % P;
     const int64_t nk = a.ntiles > blockIdx.x ? (a.ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const TwDirect<T> tw{reinterpret_cast<const vec2_t<T> *>(a.tw), LOGN};
+    const TwCat<T> tw{reinterpret_cast<const vec2_t<T> *>(a.tw)};
     const T scale = (T)a.scale;
     const bool do_scale = a.scale_out != 0;
 
@@ -211,15 +211,15 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                     vr[u * RP + r] = lds_at<T>(inr, swz<T, N>(sl, e));                               \
                     vi[u * RP + r] = lds_at<T>(ini, swz<T, N>(sl, e));                               \
                 } else {                                                                             \
-                    vr[u * RP + r] = exr[e + (e >> LR)];                                             \
-                    vi[u * RP + r] = exi[e + (e >> LR)];                                             \
+                    vr[u * RP + r] = exr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];                    \
+                    vi[u * RP + r] = exi[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];                    \
                 }                                                                                    \
             }                                                                                        \
         }                                                                                            \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
         {                                                                                            \
             const int j = t + P * u;                                                                 \
-            dit_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (int64_t)(j & (ns - 1)), tw);            \
+            dit_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (j & (ns - 1)), tw);            \
         }                                                                                            \
         if (p < NPASS - 1) {                                                                         \
             if (p > 0) __syncthreads();                                                              \
@@ -230,8 +230,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                 _Pragma("unroll") for (int f = 0; f < RP; ++f)                                       \
                 {                                                                                    \
                     const int e = base + ns * f;                                                     \
-                    exr[e + (e >> LR)] = vr[u * RP + brev(f, KP)];                                   \
-                    exi[e + (e >> LR)] = vi[u * RP + brev(f, KP)];                                   \
+                    exr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = vr[u * RP + brev(f, KP)];              \
+                    exi[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = vi[u * RP + brev(f, KP)];              \
                 }                                                                                    \
             }                                                                                        \
             if (p == 0) {                                                                            \
@@ -292,15 +292,15 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                     vr[d] = lds_at<T>(inr, swz<T, N>(sl, e));                                        \
                     vi[d] = lds_at<T>(ini, swz<T, N>(sl, e));                                        \
                 } else {                                                                             \
-                    vr[d] = exr[e + (e >> LR)];                                                      \
-                    vi[d] = exi[e + (e >> LR)];                                                      \
+                    vr[d] = exr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];                                 \
+                    vi[d] = exi[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];                                 \
                 }                                                                                    \
             }                                                                                        \
         }                                                                                            \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
         {                                                                                            \
             const int j = t + P * u;                                                                 \
-            dif_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (int64_t)(j & (ns - 1)), tw);            \
+            dif_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (j & (ns - 1)), tw);            \
         }                                                                                            \
         if (p > 0) {                                                                                 \
             if (q > 0) __syncthreads();                                                              \
@@ -310,8 +310,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                 _Pragma("unroll") for (int r = 0; r < RP; ++r)                                       \
                 {                                                                                    \
                     const int e = j + r * (N / RP);                                                  \
-                    exr[e + (e >> LR)] = vr[u * RP + r];                                             \
-                    exi[e + (e >> LR)] = vi[u * RP + r];                                             \
+                    exr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = vr[u * RP + r];                    \
+                    exi[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = vi[u * RP + r];                    \
                 }                                                                                    \
             }                                                                                        \
             if (q == 0) {                                                                            \
