@@ -116,6 +116,31 @@ int sfft_exec_interleaved(const sfft_plan *plan, const void *x, void *y,
                           int64_t batch, int64_t in_stride, int64_t out_stride,
                           int direction, void *workspace, void *stream);
 
+/* ---- one transform sharded over nranks GPUs (four-step, one all-to-all) ----
+ * N = 2^log2n = N1 * N2 with N1 = 2^floor(log2n/2).  Data distribution
+ * (G = nranks, power of two; rank g):
+ *   input   x[n], n = N2*n1 + n2, on rank g = n2 / (N2/G), local [n1][n2 % (N2/G)]
+ *   output  X[k], k = k1 + N1*k2, on rank h = k1 / (N1/G), local [k2][k1 % (N1/G)]
+ * phase 0 runs stages 1..log2 N1 (length-N1 transforms of the local columns)
+ * and writes the all-to-all SEND buffer [dest rank][n2 local][k1 local]
+ * (G contiguous segments of N/G^2 elements per plane); after an all-to-all of
+ * both planes (segment r of rank g -> slot g of rank r's RECV buffer) phase 1
+ * runs stages log2 N1 + 1 .. log2n on the RECV buffer and writes the local
+ * output.  DIT only; the inverse swaps channels at phase 0 input and phase 1
+ * output (transform.py:286-298).  Same arithmetic as the single-GPU plan. */
+typedef struct sfft_dist_plan sfft_dist_plan;
+int sfft_dist_plan_create(int log2n, int dtype, int nranks, int rank,
+                          int device, sfft_dist_plan **out);
+int sfft_dist_plan_destroy(sfft_dist_plan *plan);
+/* elements per rank (N/G), log2 N1, elements per all-to-all segment (N/G^2) */
+int sfft_dist_layout(const sfft_dist_plan *plan, int64_t *local_elems,
+                     int *log2n1, int64_t *segment_elems);
+int sfft_dist_workspace_bytes(const sfft_dist_plan *plan, size_t *bytes);
+int sfft_dist_exec_phase(const sfft_dist_plan *plan, int phase,
+                         const void *x_re, const void *x_im, void *y_re,
+                         void *y_im, int direction, void *workspace,
+                         void *stream);
+
 /* Host-only helpers (no GPU needed). */
 
 /* Stage-m factor table w[q] = cos - j sin of 2 pi q / 2^m, snapped, for

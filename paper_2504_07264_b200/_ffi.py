@@ -38,6 +38,11 @@ SIGNATURES = {
     "sfft_twiddle_table": (_I, [_I, _P, _P]),
     "sfft_count_flops": (_I, [_I, ctypes.POINTER(_I64)]),
     "sfft_launch_count": (_I64, []),
+    "sfft_dist_plan_create": (_I, [_I, _I, _I, _I, _I, ctypes.POINTER(_P)]),
+    "sfft_dist_plan_destroy": (_I, [_P]),
+    "sfft_dist_layout": (_I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I), ctypes.POINTER(_I64)]),
+    "sfft_dist_workspace_bytes": (_I, [_P, ctypes.POINTER(ctypes.c_size_t)]),
+    "sfft_dist_exec_phase": (_I, [_P, _I, _P, _P, _P, _P, _I, _P, _P]),
 }
 
 

@@ -358,6 +358,8 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         a.coarse = p->d_coarse;
         a.coarse_log = p->coarse_log;
         a.fine = p->d_fine;
+        a.jb = 0;
+        a.in_map.b = a.out_map.b = 0;
         const int64_t grid = batch * ((n >> gr.L) / TJ);
         cudaError_t e = fn(a, p->algo == SFFT_DIF, first && il, last && il, grid, st);
         if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");
@@ -530,6 +532,157 @@ int sfft_exec_interleaved(const sfft_plan *plan, const void *x, void *y, int64_t
 {
     return exec_common(plan, x, nullptr, y, nullptr, true, batch, in_stride, out_stride, direction, workspace,
                        stream);
+}
+
+/* ---------------- sharded four-step (one transform over nranks GPUs) ------------- */
+
+struct sfft_dist_plan {
+    sfft_plan *base = nullptr;   // tables of the full-size plan
+    int nranks = 1, rank = 0, logg = 0, L1 = 0;
+    std::vector<Group> ga, gb;   // phase 0: stages 1..L1, phase 1: L1+1..m
+};
+
+static std::vector<Group> split_range(int S0, int L)
+{
+    const int G = (L + kPassMaxL - 1) / kPassMaxL;
+    std::vector<Group> g;
+    int S = S0;
+    for (int k = 0; k < G; ++k) {
+        int l = L / G + (k < L % G ? 1 : 0);
+        g.push_back({S, l});
+        S += l;
+    }
+    return g;
+}
+
+int sfft_dist_plan_create(int log2n, int dtype, int nranks, int rank, int device, sfft_dist_plan **out)
+{
+    if (!out) return fail(SFFT_EINVAL, "out is NULL");
+    *out = nullptr;
+    if (nranks < 1 || (nranks & (nranks - 1)))
+        return fail(SFFT_EINVAL, "nranks must be a power of two >= 1, got %d", nranks);
+    if (rank < 0 || rank >= nranks) return fail(SFFT_EINVAL, "rank %d out of range for %d ranks", rank, nranks);
+    int logg = 0;
+    while ((1 << logg) < nranks) ++logg;
+    if (log2n < 0) return fail(SFFT_EINVAL, "stage count m must be >= 0, got %d", log2n);
+    if (log2n > SFFT_MAX_LOG2N)
+        return fail(SFFT_ECAPACITY, "m=%d exceeds the plan limit max_m=%d", log2n, SFFT_MAX_LOG2N);
+    if (dtype != SFFT_F32 && dtype != SFFT_F64) return fail(SFFT_EINVAL, "unknown dtype %d", dtype);
+    const int tjlog = dtype == SFFT_F32 ? 5 : 4;
+    const int L1 = log2n / 2, L2 = log2n - L1;
+    if (L1 < kPassMinL || L1 - logg < tjlog || L2 - logg < tjlog)
+        return fail(SFFT_ECAPACITY, "a sharded transform over %d ranks needs log2n >= %d, got %d", nranks,
+                    2 * (tjlog + logg > kPassMinL ? tjlog + logg : kPassMinL), log2n);
+    // the full-size plan provides the stage tables (stage-major up to its
+    // cat_top, which covers every stage for log2n <= 12)
+    sfft_plan *base = nullptr;
+    int rc = sfft_plan_create_ex(log2n, dtype, SFFT_DIT, device, SFFT_MAX_LOG2N, 0, SFFT_KERNEL_AUTO, &base);
+    if (rc) return rc;
+    sfft_dist_plan *d = new sfft_dist_plan;
+    d->base = base;
+    d->nranks = nranks;
+    d->rank = rank;
+    d->logg = logg;
+    d->L1 = L1;
+    d->ga = split_range(0, L1);
+    d->gb = split_range(L1, L2);
+    *out = d;
+    return SFFT_OK;
+}
+
+int sfft_dist_plan_destroy(sfft_dist_plan *d)
+{
+    if (!d) return SFFT_OK;
+    sfft_plan_destroy(d->base);
+    delete d;
+    return SFFT_OK;
+}
+
+int sfft_dist_layout(const sfft_dist_plan *d, int64_t *local_elems, int *log2n1, int64_t *segment_elems)
+{
+    if (!d) return fail(SFFT_EINVAL, "plan is NULL");
+    const int64_t n = int64_t(1) << d->base->log2n;
+    if (local_elems) *local_elems = n >> d->logg;
+    if (log2n1) *log2n1 = d->L1;
+    if (segment_elems) *segment_elems = n >> (2 * d->logg);
+    return SFFT_OK;
+}
+
+int sfft_dist_workspace_bytes(const sfft_dist_plan *d, size_t *bytes)
+{
+    if (!d || !bytes) return fail(SFFT_EINVAL, "NULL argument");
+    const size_t esz = d->base->dtype == SFFT_F32 ? 4 : 8;
+    *bytes = 4 * ((size_t)1 << (d->base->log2n - d->logg)) * esz;
+    return SFFT_OK;
+}
+
+int sfft_dist_exec_phase(const sfft_dist_plan *d, int phase, const void *x_re, const void *x_im, void *y_re,
+                         void *y_im, int direction, void *workspace, void *stream)
+{
+    if (!d) return fail(SFFT_EINVAL, "plan is NULL");
+    if (phase != 0 && phase != 1) return fail(SFFT_EINVAL, "phase must be 0 or 1, got %d", phase);
+    if (direction != SFFT_FORWARD && direction != SFFT_INVERSE)
+        return fail(SFFT_EINVAL, "direction must be -1 (forward) or +1 (inverse), got %d", direction);
+    if (!x_re || !x_im || !y_re || !y_im) return fail(SFFT_EINVAL, "NULL signal pointer");
+    const std::vector<Group> &gs = phase == 0 ? d->ga : d->gb;
+    if (gs.size() > 1 && !workspace) return fail(SFFT_EINVAL, "this phase needs a workspace (sfft_dist_workspace_bytes)");
+    const sfft_plan *p = d->base;
+    DeviceGuard dg(p->device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    const int m = p->log2n, b = d->logg, L1 = d->L1;
+    const int64_t n = int64_t(1) << m, nl = n >> b;
+    const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
+    char *ws = (char *)workspace;
+    void *bufA[2] = {ws, ws + nl * esz};
+    void *bufB[2] = {ws + 2 * nl * esz, ws + 3 * nl * esz};
+    const bool inv = direction == SFFT_INVERSE;
+    const int TJ = pass_tile(p->dtype);
+    const int G = (int)gs.size();
+    for (int k = 0; k < G; ++k) {
+        const Group gr = gs[k];
+        PassLaunchFn fn = pass_launcher(p->dtype, gr.L);
+        if (!fn) return fail(SFFT_EINVAL, "no pass kernel for L=%d", gr.L);
+        PassArgs a;
+        memset(&a, 0, sizeof a);
+        const bool first = k == 0, last = k == G - 1;
+        void **src = (k % 2 == 1) ? bufA : bufB;
+        void **dst = (k % 2 == 0) ? bufA : bufB;
+        a.x0 = first ? x_re : src[0];
+        a.x1 = first ? x_im : src[1];
+        a.y0 = last ? y_re : dst[0];
+        a.y1 = last ? y_im : dst[1];
+        a.batch = 1;
+        a.in_stride = a.out_stride = nl;
+        a.m = m;
+        a.S = gr.S;
+        a.swap_in = phase == 0 && first && inv;
+        a.swap_out = phase == 1 && last && inv;
+        a.scale = (phase == 1 && last && inv) ? 1.0 / (double)n : 1.0;
+        a.tw = p->d_tw;
+        a.tw_cat_top = p->cat_top;
+        a.tw_top_tab = p->d_top;
+        a.coarse = p->d_coarse;
+        a.coarse_log = p->coarse_log;
+        a.fine = p->d_fine;
+        a.jb = b;
+        a.jrank = d->rank;
+        if (phase == 0) {
+            // owner field = top b bits of the column index n2 = (index >> s) mod 2^(m-L1)
+            a.jpos = gr.S + (m - L1) - b;
+            a.in_map = {b, gr.S + (m - L1) - b, -1, m - b};
+            if (last) a.out_map = {b, m - b, L1 - b, m - b};   // send layout [dest][n2_local][k1_local]
+            else a.out_map = {b, gr.S + gr.L + (m - L1) - b, -1, m - b};
+        } else {
+            // owner field = top b bits of k1 = index mod 2^L1
+            a.jpos = L1 - b;
+            a.in_map = {b, L1 - b, -1, m - b};
+            a.out_map = {b, L1 - b, -1, m - b};
+        }
+        const int64_t grid = ((n >> gr.L) >> b) / TJ;
+        cudaError_t e = fn(a, false, false, false, grid, (cudaStream_t)stream);
+        if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch (sharded)");
+    }
+    return SFFT_OK;
 }
 
 }  // extern "C"

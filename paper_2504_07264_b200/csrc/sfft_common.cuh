@@ -157,7 +157,9 @@ template <> struct SkipTrivial<float> { static constexpr bool value = true; };
 // register rev_K(f) holds output frequency f.  Validated bitwise against the
 // reference by tests/test_schedule_model.py (a numpy restatement of exactly
 // this index map).
-template <typename T, int K, typename TW>
+// TRIV = false promises gs >= 1 and no trivial factors to skip (every pass
+// group after the first), which removes the per-stage kind tests.
+template <typename T, int K, bool TRIV = true, typename TW>
 __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw)
 {
     using I = typename TW::index_t;
@@ -169,7 +171,8 @@ __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::in
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;
             // 0: stage 1 (no factor), 1: identity, 2: quarter turn, 3: generic
-            const int kind = i == 1 ? 0
+            const int kind = !TRIV ? 3
+                           : i == 1 ? 0
                            : (SkipTrivial<T>::value && gs == 0 && f == 0) ? 1
                            : (SkipTrivial<T>::value && gs == 0 && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w;
@@ -198,7 +201,7 @@ __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::in
 
 // Transpose of dit_stages: DIF stages gs+K .. gs+1 (descending), same
 // register map run backwards.
-template <typename T, int K, typename TW>
+template <typename T, int K, bool TRIV = true, typename TW>
 __device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw)
 {
     using I = typename TW::index_t;
@@ -209,7 +212,8 @@ __device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, typename TW::in
 #pragma unroll
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;
-            const int kind = i == 1 ? 0
+            const int kind = !TRIV ? 3
+                           : i == 1 ? 0
                            : (SkipTrivial<T>::value && gs == 0 && f == 0) ? 1
                            : (SkipTrivial<T>::value && gs == 0 && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w;

@@ -21,7 +21,7 @@ using TmaLaunchFn = cudaError_t (*)(const TmaLaunch &L, cudaStream_t st);
 
 constexpr int kFusedMaxLog = 12;
 constexpr int kMaxRadixLog = 5;
-constexpr int kPassMinL = 5, kPassMaxL = 8;
+constexpr int kPassMinL = 4, kPassMaxL = 9;
 
 // Registry lookups (nullptr when the combination was not instantiated).
 // dtype: 0 = f32, 1 = f64.  Interleaved variants exist only for the

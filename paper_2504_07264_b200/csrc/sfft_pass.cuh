@@ -3,8 +3,8 @@
 // Replaces the reference's cache-blocked wide-stage executor
 // (transform.py:219-237 segments + _dit_stage_pair slabs, :153-200) for
 // long signals.  The m stages are split into G groups of L_g <= 8
-// consecutive stages; one launch per group.  Group (S, L) treats the array
-// as N / 2^L independent 2^L-point sub-problems
+// consecutive stages; one launch per group.  Group (S, L) treats a row as
+// N / 2^L independent 2^L-point sub-problems
 //     sub-problem j:  elements  in[ j + e * N/2^L ],  e < 2^L
 //     outputs          out[ (j>>S)*2^S*2^L + (j & (2^S-1)) + 2^S * o ]
 // (DIT; DIF is the transpose, groups run last-to-first), i.e. the same
@@ -17,17 +17,44 @@
 // The only non-unit-stride global pattern (DIT group S = 0 output, DIF group
 // S = 0 input: rows of 2^L per sub-problem) goes through a shared-memory
 // transpose so that the global side is one contiguous TJ*2^L block.
+//
+// Specialisation: the group with S = 0 (template S0) is the only one whose
+// stages can be stage 1 or carry trivial factors, so every other group runs
+// with compile-time "generic factor" stages; in-row indices are 32-bit
+// (m <= 30); the owner-field address maps of a sharded transform
+// (sfft_dist_*) are compiled in only for DIST launches.
 #pragma once
 #include "sfft_common.cuh"
 
 namespace sfft {
+
+// Global Stockham index -> local address, for a rank of a sharded transform
+// (sfft_dist): remove the b-bit rank field at bit p1; optionally then move
+// the b-bit destination field at bit p2 to the top (the all-to-all send
+// layout: one contiguous segment per destination rank).
+struct AddrMap {
+    int b;      // field width (log2 ranks)
+    int p1;     // position of the owner field that is removed
+    int p2;     // position (after removal) of the destination field moved to the top, -1 = none
+    int width;  // bits of the index after removal (m - b)
+    __host__ __device__ __forceinline__ uint32_t operator()(uint32_t x) const
+    {
+        const uint32_t lo1 = x & ((1u << p1) - 1u);
+        x = ((x >> (p1 + b)) << p1) | lo1;
+        if (p2 < 0) return x;
+        const uint32_t h = (x >> p2) & ((1u << b) - 1u);
+        const uint32_t lo2 = x & ((1u << p2) - 1u);
+        const uint32_t rest = ((x >> (p2 + b)) << p2) | lo2;
+        return (h << (width - b)) | rest;
+    }
+};
 
 struct PassArgs {
     const void *x0, *x1;   // source planes (or pairs when the source is interleaved)
     void *y0, *y1;         // destination planes (or pairs)
     int64_t batch;
     int64_t in_stride, out_stride;
-    int m;                 // log2 N
+    int m;                 // log2 N (<= 30)
     int S;                 // stage offset of this group
     int swap_in, swap_out; // channel swap of the inverse (first / last launch)
     double scale;          // applied at the destination when swap_out
@@ -37,6 +64,10 @@ struct PassArgs {
     const double2 *coarse; // two-level fp32 twiddles (see TwTwoLevel)
     int coarse_log;
     const double2 *fine;
+    // sharded transforms: this launch runs the sub-problems whose index has
+    // `jrank` in the jb-bit field at bit jpos; addresses go through the maps
+    int jb, jpos, jrank;
+    AddrMap in_map, out_map;
 };
 
 template <typename T, int L, int LR_REQ>
@@ -106,30 +137,34 @@ __device__ __forceinline__ PIO<T, IL> make_pio(const PassArgs &a)
     return p;
 }
 
-template <typename T, bool TWO>
-struct TwSel { using type = TwCatTop<T>; };
-template <typename T>
-struct TwSel<T, true> { using type = TwTwoLevel<T>; };
+// Twiddle source of a group: the S = 0 group only touches stages <= 8, all in
+// the stage-major table; later groups may need the large-stage sources.
+template <typename T, bool S0> struct PassTw { using type = TwCatTop<T>; };
+template <> struct PassTw<float, false> { using type = TwTwoLevel<float>; };
+template <> struct PassTw<float, true> { using type = TwCat<float>; };
+template <> struct PassTw<double, true> { using type = TwCat<double>; };
 
-template <typename T, bool TWO>
-__device__ __forceinline__ typename TwSel<T, TWO>::type make_tw(const PassArgs &a)
+template <typename T, bool S0>
+__device__ __forceinline__ typename PassTw<T, S0>::type make_pass_tw(const PassArgs &a)
 {
-    typename TwSel<T, TWO>::type tw;
+    typename PassTw<T, S0>::type tw;
     tw.tab = (const vec2_t<T> *)a.tw;
-    tw.cat_top = a.tw_cat_top;
-    if constexpr (!TWO) {
-        tw.top_tab = (const vec2_t<T> *)a.tw_top_tab;
-        tw.top = a.m;
-    } else {
-        tw.coarse = a.coarse;
-        tw.coarse_log = a.coarse_log;
-        tw.fine = a.fine;
-        tw.m = a.m;
+    if constexpr (!S0) {
+        tw.cat_top = a.tw_cat_top;
+        if constexpr (sizeof(T) == 8) {
+            tw.top_tab = (const vec2_t<T> *)a.tw_top_tab;
+            tw.top = a.m;
+        } else {
+            tw.coarse = a.coarse;
+            tw.coarse_log = a.coarse_log;
+            tw.fine = a.fine;
+            tw.m = a.m;
+        }
     }
     return tw;
 }
 
-template <typename T, int L, int LR_REQ, bool DIF, bool IL_IN, bool IL_OUT, bool TWO>
+template <typename T, int L, int LR_REQ, bool DIF, bool IL_IN, bool IL_OUT, bool S0, bool DIST>
 __global__ void __launch_bounds__(PassShape<T, L, LR_REQ>::NT)
 sfft_pass_kernel(const PassArgs a)
 {
@@ -140,26 +175,33 @@ sfft_pass_kernel(const PassArgs a)
     T *sr = reinterpret_cast<T *>(smem_raw);
     T *si = sr + SUB * RS;
 
-    const int m = a.m, S = a.S;
-    const int64_t NJ = int64_t(1) << (m - L);         // sub-problems per row
-    const int64_t tiles = NJ / TJ;
-    const int64_t row = (int64_t)blockIdx.x / tiles;
-    const int64_t j0 = ((int64_t)blockIdx.x % tiles) * TJ;
+    const int m = a.m;
+    const int S = S0 ? 0 : a.S;
+    const uint32_t NJ = 1u << (m - L);                  // sub-problems per row (global)
+    const uint32_t tiles = (NJ >> (DIST ? a.jb : 0)) / TJ;
+    const int64_t row = (int64_t)(blockIdx.x / tiles);
+    uint32_t j0 = (blockIdx.x % tiles) * TJ;
+    if constexpr (DIST) {   // insert the rank field (jpos >= log2 TJ keeps a tile contiguous)
+        const uint32_t lo = j0 & ((1u << a.jpos) - 1u);
+        j0 = ((j0 >> a.jpos) << (a.jpos + a.jb)) | ((uint32_t)a.jrank << a.jpos) | lo;
+    }
     const int tid = threadIdx.x;
     const int jl = tid % TJ, t = tid / TJ;
-    const int64_t j = j0 + jl;
-    const int64_t ns = int64_t(1) << S;
-    const int64_t c = j & (ns - 1);
-    const int64_t gbase = (j >> S) * ns * SUB + c;     // destination (DIT) / source (DIF) of o: gbase + ns*o
+    const uint32_t j = j0 + jl;
+    const uint32_t ns = 1u << S;
+    const uint32_t c = j & (ns - 1u);
+    const uint32_t gbase = (j >> S) * ns * SUB + c;     // DIT destination / DIF source of o: gbase + ns*o
     const int64_t ioff = row * a.in_stride, ooff = row * a.out_stride;
+    const AddrMap imap = a.in_map, omap = a.out_map;
+    auto iaddr = [&](uint32_t x) -> int64_t { return ioff + (DIST ? imap(x) : x); };
+    auto oaddr = [&](uint32_t x) -> int64_t { return ooff + (DIST ? omap(x) : x); };
 
     const PIO<T, IL_IN> src = make_pio<T, IL_IN>(a);
     const PIO<T, IL_OUT> dst = make_pio<T, IL_OUT>(a);
-    const auto tw = make_tw<T, TWO>(a);
+    const auto tw = make_pass_tw<T, S0>(a);
+    using I = typename PassTw<T, S0>::type::index_t;
     const bool swap_in = a.swap_in != 0, swap_out = a.swap_out != 0;
     const T scale = (T)a.scale;
-
-    T vr[R], vi[R];
 
     auto put_out = [&](int64_t off, T re, T im) {
         if (swap_out) dst.store(off, im * scale, re * scale);
@@ -172,15 +214,16 @@ sfft_pass_kernel(const PassArgs a)
         im = swap_in ? x : y;
     };
 
+    T vr[R], vi[R];
+
     if constexpr (!DIF) {
         // ------------------------------ DIT ------------------------------
 #pragma unroll
         for (int pp = 0; pp < NPI; ++pp) {
             const int sp = pp * LR;
             const int kp = cmin(LR, L - sp);
-            // kp is a compile-time constant after unrolling; dispatch on it
 #define SFFT_DIT_INTERNAL(KP)                                                                   \
-    if constexpr (KP <= LR) if (kp == KP) {                                                                             \
+    if constexpr (KP <= LR) if (kp == KP) {                                                     \
         constexpr int RP = 1 << KP, U = R / RP;                                                 \
         const int nsp = 1 << sp;                                                                \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                           \
@@ -189,7 +232,7 @@ sfft_pass_kernel(const PassArgs a)
             _Pragma("unroll") for (int r = 0; r < RP; ++r)                                      \
             {                                                                                   \
                 const int e = jp + r * (SUB / RP);                                              \
-                if (pp == 0) get_in(ioff + j + (int64_t)e * NJ, vr[u * RP + r], vi[u * RP + r]); \
+                if (pp == 0) get_in(iaddr(j + (uint32_t)e * NJ), vr[u * RP + r], vi[u * RP + r]); \
                 else {                                                                          \
                     vr[u * RP + r] = sr[e * RS + jl];                                           \
                     vi[u * RP + r] = si[e * RS + jl];                                           \
@@ -199,11 +242,11 @@ sfft_pass_kernel(const PassArgs a)
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                           \
         {                                                                                       \
             const int jp = t + P * u;                                                           \
-            dit_stages<T, KP>(vr + u * RP, vi + u * RP, S + sp,                                 \
-                              c + ((int64_t)(jp & (nsp - 1)) << S), tw);                        \
+            dit_stages<T, KP, S0>(vr + u * RP, vi + u * RP, S + sp,                             \
+                                  (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw);              \
         }                                                                                       \
         const bool last = pp == NPI - 1;                                                        \
-        if (!last || S == 0) {                                                                  \
+        if (!last || S0) {                                                                      \
             if (pp > 0) __syncthreads();                                                        \
             _Pragma("unroll") for (int u = 0; u < U; ++u)                                       \
             {                                                                                   \
@@ -223,8 +266,8 @@ sfft_pass_kernel(const PassArgs a)
                 const int jp = t + P * u;                                                       \
                 _Pragma("unroll") for (int f = 0; f < RP; ++f)                                  \
                 {                                                                               \
-                    const int o = jp + nsp * f;                                                 \
-                    put_out(ooff + gbase + ns * o, vr[u * RP + brev(f, KP)],                    \
+                    const uint32_t o = jp + nsp * f;                                            \
+                    put_out(oaddr(gbase + ns * o), vr[u * RP + brev(f, KP)],                    \
                             vi[u * RP + brev(f, KP)]);                                          \
                 }                                                                               \
             }                                                                                   \
@@ -237,24 +280,24 @@ sfft_pass_kernel(const PassArgs a)
             SFFT_DIT_INTERNAL(5)
 #undef SFFT_DIT_INTERNAL
         }
-        if (S == 0) {
+        if constexpr (S0) {
             // outputs of this tile are the contiguous rows j0..j0+TJ of 2^L:
             // copy smem [o][jl] -> global in linear order
-            const int64_t obase = ooff + j0 * SUB;
+            const uint32_t obase = j0 * SUB;
             for (int k = tid; k < TJ * SUB; k += NT) {
                 const int jj = k >> L, o = k & (SUB - 1);
-                put_out(obase + k, sr[o * RS + jj], si[o * RS + jj]);
+                put_out(oaddr(obase + k), sr[o * RS + jj], si[o * RS + jj]);
             }
         }
     } else {
         // ------------------------------ DIF ------------------------------
-        if (S == 0) {
+        if constexpr (S0) {
             // inputs are the contiguous rows j0..j0+TJ of 2^L: stage them
-            const int64_t ibase = ioff + j0 * SUB;
+            const uint32_t ibase = j0 * SUB;
             for (int k = tid; k < TJ * SUB; k += NT) {
                 const int jj = k >> L, o = k & (SUB - 1);
                 T re, im;
-                get_in(ibase + k, re, im);
+                get_in(iaddr(ibase + k), re, im);
                 sr[o * RS + jj] = re;
                 si[o * RS + jj] = im;
             }
@@ -265,7 +308,7 @@ sfft_pass_kernel(const PassArgs a)
             const int sp = pp * LR;
             const int kp = cmin(LR, L - sp);
 #define SFFT_DIF_INTERNAL(KP)                                                                   \
-    if constexpr (KP <= LR) if (kp == KP) {                                                                             \
+    if constexpr (KP <= LR) if (kp == KP) {                                                     \
         constexpr int RP = 1 << KP, U = R / RP;                                                 \
         const int nsp = 1 << sp;                                                                \
         const bool first = pp == NPI - 1;                                                       \
@@ -277,7 +320,7 @@ sfft_pass_kernel(const PassArgs a)
             {                                                                                   \
                 const int e = base + nsp * f;                                                   \
                 const int d = u * RP + brev(f, KP);                                             \
-                if (first && S != 0) get_in(ioff + gbase + ns * e, vr[d], vi[d]);               \
+                if (first && !S0) get_in(iaddr(gbase + ns * (uint32_t)e), vr[d], vi[d]);        \
                 else {                                                                          \
                     vr[d] = sr[e * RS + jl];                                                    \
                     vi[d] = si[e * RS + jl];                                                    \
@@ -287,11 +330,11 @@ sfft_pass_kernel(const PassArgs a)
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                           \
         {                                                                                       \
             const int jp = t + P * u;                                                           \
-            dif_stages<T, KP>(vr + u * RP, vi + u * RP, S + sp,                                 \
-                              c + ((int64_t)(jp & (nsp - 1)) << S), tw);                        \
+            dif_stages<T, KP, S0>(vr + u * RP, vi + u * RP, S + sp,                             \
+                                  (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw);              \
         }                                                                                       \
         if (pp != 0) {                                                                          \
-            if (!first || S == 0) __syncthreads();                                              \
+            if (!first || S0) __syncthreads();                                                  \
             _Pragma("unroll") for (int u = 0; u < U; ++u)                                       \
             {                                                                                   \
                 const int jp = t + P * u;                                                       \
@@ -310,7 +353,7 @@ sfft_pass_kernel(const PassArgs a)
                 _Pragma("unroll") for (int r = 0; r < RP; ++r)                                  \
                 {                                                                               \
                     const int e = jp + r * (SUB / RP);                                          \
-                    put_out(ooff + j + (int64_t)e * NJ, vr[u * RP + r], vi[u * RP + r]);        \
+                    put_out(oaddr(j + (uint32_t)e * NJ), vr[u * RP + r], vi[u * RP + r]);       \
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \

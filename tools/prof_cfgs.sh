@@ -1,9 +1,10 @@
-set -x
-for C in cfg3_n1024_f32 cfg3_n1024_f64 cfg4_n4096_f32; do
-  CMD="python bench.py --config $C --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
-  $CMD > gpurun_out/plain_$C.log 2>&1 || exit 1
+# usage: bash tools/prof_cfgs.sh TAG cfg...   (ncu --set full of the top kernel per config)
+TAG=$1; shift
+for C in "$@"; do
+  CMD="python bench.py --config $C --steps 3 --warmup 2 --no-e2e --no-cpu-baseline"
+  $CMD > gpurun_out/plain_${TAG}_$C.log 2>&1 || { echo "plain run failed: $C"; exit 1; }
 done
-for C in cfg3_n1024_f32 cfg3_n1024_f64 cfg4_n4096_f32; do
-  CMD="python bench.py --config $C --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
-  ncu --set full --clock-control none --import-source on -k regex:sfft -s 1 -c 1 -o gpurun_out/prof_$C $CMD > gpurun_out/ncu_$C.log 2>&1
+for C in "$@"; do
+  CMD="python bench.py --config $C --steps 3 --warmup 2 --no-e2e --no-cpu-baseline"
+  ncu --set full --clock-control none --import-source on -k regex:sfft -s 2 -c 1 -o gpurun_out/prof_${TAG}_$C $CMD > gpurun_out/ncu_${TAG}_$C.log 2>&1
 done
