@@ -15,6 +15,7 @@
 #include <stdint.h>
 
 #include "sfft_layouts.h"
+#include "sfft_small_tw.h"
 
 namespace sfft {
 
@@ -149,6 +150,22 @@ __host__ __device__ constexpr int ex_sstr()
 template <typename T> struct SkipTrivial { static constexpr bool value = false; };
 template <> struct SkipTrivial<float> { static constexpr bool value = true; };
 
+// Stage-t factors, t <= 5, as immediates (index 2^(t-1)-1+f); bitwise the
+// table values (generated from the same formula, sfft_small_tw.h).
+template <typename T> struct SmallTw;
+template <> struct SmallTw<float> {
+    static __device__ __forceinline__ float2 get(int k) { return make_float2(small_tw_re32(k), small_tw_im32(k)); }
+};
+template <> struct SmallTw<double> {
+    static __device__ __forceinline__ double2 get(int k) { return make_double2(small_tw_re64(k), small_tw_im64(k)); }
+};
+
+// fp32 forms the 2^(t-1) factors of a stage from ONE table/two-level lookup:
+// w_i(c + f 2^gs) = w_i(c) * w_{2^t}^f (t = i - gs), the second factor an
+// immediate.  fp64 reads every factor from the table (bit-exact contract).
+template <typename T> struct FactorTw { static constexpr bool value = false; };
+template <> struct FactorTw<float> { static constexpr bool value = true; };
+
 // K consecutive DIT stages (global stages gs+1 .. gs+K) on the 2^K values
 // v[0..2^K) of one virtual thread.  Register position p holds, before stage
 // t, the (size 2^(gs+t-1)) partial transform of sub-sequence (p mod
@@ -163,20 +180,36 @@ template <typename T, int K, bool TRIV = true, typename TW>
 __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw)
 {
     using I = typename TW::index_t;
+    const bool first = TRIV && gs == 0;   // first pass: every factor is a compile-time constant
 #pragma unroll
     for (int t = 1; t <= K; ++t) {
         const int half = (1 << K) >> t;
         const int i = gs + t;
+        vec2_t<T> base;
+        if (!first && FactorTw<T>::value) base = tw.get(i, cbase);
 #pragma unroll
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;
             // 0: stage 1 (no factor), 1: identity, 2: quarter turn, 3: generic
             const int kind = !TRIV ? 3
                            : i == 1 ? 0
-                           : (SkipTrivial<T>::value && gs == 0 && f == 0) ? 1
-                           : (SkipTrivial<T>::value && gs == 0 && (f << 2) == (1 << t)) ? 2 : 3;
+                           : (SkipTrivial<T>::value && first && f == 0) ? 1
+                           : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w;
-            if (kind == 3) w = tw.get(i, cbase + ((I)f << gs));
+            if (kind == 3) {
+                if (first) {
+                    w = SmallTw<T>::get((1 << (t - 1)) - 1 + f);
+                } else if (FactorTw<T>::value) {
+                    if (f == 0) {
+                        w = base;
+                    } else {
+                        const vec2_t<T> s = SmallTw<T>::get((1 << (t - 1)) - 1 + f);
+                        cmul(base.x, base.y, s.x, s.y, w.x, w.y);
+                    }
+                } else {
+                    w = tw.get(i, cbase + ((I)f << gs));
+                }
+            }
 #pragma unroll
             for (int r = 0; r < half; ++r) {
                 const int p1 = r + rf, p2 = p1 + half;
@@ -205,19 +238,35 @@ template <typename T, int K, bool TRIV = true, typename TW>
 __device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw)
 {
     using I = typename TW::index_t;
+    const bool first = TRIV && gs == 0;
 #pragma unroll
     for (int t = K; t >= 1; --t) {
         const int half = (1 << K) >> t;
         const int i = gs + t;
+        vec2_t<T> base;
+        if (!first && FactorTw<T>::value) base = tw.get(i, cbase);
 #pragma unroll
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;
             const int kind = !TRIV ? 3
                            : i == 1 ? 0
-                           : (SkipTrivial<T>::value && gs == 0 && f == 0) ? 1
-                           : (SkipTrivial<T>::value && gs == 0 && (f << 2) == (1 << t)) ? 2 : 3;
+                           : (SkipTrivial<T>::value && first && f == 0) ? 1
+                           : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w;
-            if (kind == 3) w = tw.get(i, cbase + ((I)f << gs));
+            if (kind == 3) {
+                if (first) {
+                    w = SmallTw<T>::get((1 << (t - 1)) - 1 + f);
+                } else if (FactorTw<T>::value) {
+                    if (f == 0) {
+                        w = base;
+                    } else {
+                        const vec2_t<T> s = SmallTw<T>::get((1 << (t - 1)) - 1 + f);
+                        cmul(base.x, base.y, s.x, s.y, w.x, w.y);
+                    }
+                } else {
+                    w = tw.get(i, cbase + ((I)f << gs));
+                }
+            }
 #pragma unroll
             for (int r = 0; r < half; ++r) {
                 const int p1 = r + rf, p2 = p1 + half;

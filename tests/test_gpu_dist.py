@@ -65,8 +65,12 @@ def test_sharded_f32_matches_single_gpu(cuda, m, world):
     wr, wi = oracle.fft_split_c(xr, xi)
     err = np.sqrt(np.sum((gr - wr) ** 2 + (gi - wi) ** 2) / np.sum(wr ** 2 + wi ** 2))
     assert err <= 1e-5 * m
+    # the single-GPU schedule groups the stages differently, and fp32 forms
+    # factors per group (w_i(c) * w_{2^t}^f), so agreement is to rounding
     sr, si = sf.fft_split(torch.from_numpy(xr).cuda(), torch.from_numpy(xi).cuda())
-    assert np.array_equal(sr.cpu().numpy(), gr) and np.array_equal(si.cpu().numpy(), gi)
+    sr, si = sr.cpu().numpy().astype(np.float64), si.cpu().numpy().astype(np.float64)
+    d = np.sqrt(np.sum((sr - gr) ** 2 + (si - gi) ** 2) / np.sum(sr ** 2 + si ** 2))
+    assert d <= 1e-6
 
 
 def test_sharded_plan_limits(cuda):
