@@ -262,25 +262,78 @@ def fft_split(x_re, x_im, *, algorithm="dit", inverse: bool = False, out=None, p
         _exec_split_device(plan, xr, xi, yr, yi, inverse)
         return yr, yi
 
-    # host buffers: H2D, GPU transform, D2H (the e2e path of bench.py)
-    with torch.cuda.device(device):
-        xr = sig.re.to(device, non_blocking=True)
-        xi = sig.im.to(device, non_blocking=True)
-        yr, yi = torch.empty_like(xr), torch.empty_like(xi)
-        _exec_split_device(plan, xr, xi, yr, yi, inverse)
-        if out is not None:
-            hr, hi = out
-            hr, hi = (torch.from_numpy(hr) if not isinstance(hr, torch.Tensor) else hr,
-                      torch.from_numpy(hi) if not isinstance(hi, torch.Tensor) else hi)
-            hr.copy_(yr, non_blocking=True)
-            hi.copy_(yi, non_blocking=True)
-            torch.cuda.current_stream(device).synchronize()
-            return out
-        hr = yr.to("cpu")
-        hi = yi.to("cpu")
+    # host buffers: chunked H2D -> transform -> D2H pipeline (the e2e path)
+    hr_in, hi_in = sig.re, sig.im
+    if out is not None:
+        hr, hi = out
+        hr = torch.from_numpy(hr) if not isinstance(hr, torch.Tensor) else hr
+        hi = torch.from_numpy(hi) if not isinstance(hi, torch.Tensor) else hi
+        if hr.shape != hr_in.shape or hi.shape != hr_in.shape or hr.dtype != hr_in.dtype:
+            raise ValueError("out planes must match the input shape and dtype")
+    else:
+        pin = hr_in.is_pinned()
+        hr = torch.empty(hr_in.shape, dtype=hr_in.dtype, pin_memory=pin)
+        hi = torch.empty(hr_in.shape, dtype=hr_in.dtype, pin_memory=pin)
+    _host_pipeline(plan, device, hr_in, hi_in, hr, hi, inverse)
+    if out is not None:
+        return out
     if was_numpy:
         return hr.numpy(), hi.numpy()
     return hr, hi
+
+
+_PIPE_CHUNK_BYTES = 8 << 20    # per plane per chunk (tools/e2e_probe.py sweep)
+_PIPE_SLOTS = 4
+
+
+def _host_pipeline(plan, device, hr_in, hi_in, hr_out, hi_out, inverse):
+    """Host planes -> device -> transform -> host planes, in row chunks on
+    three streams (H2D, compute, D2H) so that both PCIe directions and the
+    kernel overlap; with pinned host memory every copy is asynchronous."""
+    one = hr_in.ndim == 1
+    xr2 = hr_in.reshape(1, -1) if one else hr_in
+    xi2 = hi_in.reshape(1, -1) if one else hi_in
+    yr2 = hr_out.reshape(1, -1) if one else hr_out
+    yi2 = hi_out.reshape(1, -1) if one else hi_out
+    b, n = xr2.shape
+    esz = xr2.element_size()
+    rows = max(1, min(b, _PIPE_CHUNK_BYTES // (n * esz)))
+    nchunks = (b + rows - 1) // rows
+    slots = min(_PIPE_SLOTS, nchunks)
+    with torch.cuda.device(device):
+        caller = torch.cuda.current_stream(device)
+        s_in, s_cmp, s_out = (torch.cuda.Stream(device) for _ in range(3))
+        for s_ in (s_in, s_cmp, s_out):
+            s_.wait_stream(caller)
+        bufs = [tuple(torch.empty((rows, n), dtype=xr2.dtype, device=device) for _ in range(4))
+                for _ in range(slots)]
+        freed = [None] * slots
+        for k in range(nchunks):
+            r0, r1 = k * rows, min(b, (k + 1) * rows)
+            sl = k % slots
+            dxr, dxi, dyr, dyi = (t[: r1 - r0] for t in bufs[sl])
+            with torch.cuda.stream(s_in):
+                if freed[sl] is not None:
+                    s_in.wait_event(freed[sl])
+                dxr.copy_(xr2[r0:r1], non_blocking=True)
+                dxi.copy_(xi2[r0:r1], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(s_in)
+            with torch.cuda.stream(s_cmp):
+                s_cmp.wait_event(ev_in)
+                _exec_split_device(plan, dxr, dxi, dyr, dyi, inverse)
+                ev_cmp = torch.cuda.Event()
+                ev_cmp.record(s_cmp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_cmp)
+                yr2[r0:r1].copy_(dyr, non_blocking=True)
+                yi2[r0:r1].copy_(dyi, non_blocking=True)
+                ev_out = torch.cuda.Event()
+                ev_out.record(s_out)
+                freed[sl] = ev_out
+        s_out.synchronize()
+        for s_ in (s_in, s_cmp, s_out):
+            caller.wait_stream(s_)
 
 
 def ifft_split(x_re, x_im, *, algorithm="dit", out=None, plan=None):

@@ -235,3 +235,23 @@ def test_tma_falls_back_for_unaligned_rows(cuda):
     forced = sf.make_plan(m, dtype=torch.float32, device="cuda:0", kernel="tma")
     with pytest.raises(ValueError, match="TMA kernel needs"):
         sf.fft_split(xr, xi, plan=forced)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_pipeline_many_chunks(cuda, monkeypatch, pinned):
+    # host planes go through the chunked H2D/compute/D2H pipeline; force many
+    # chunks (and a ragged last one) and compare with the device-resident path
+    from paper_2504_07264_b200 import transform
+    monkeypatch.setattr(transform, "_PIPE_CHUNK_BYTES", 64 * 4 * 1000)
+    rng = np.random.default_rng(11)
+    b, n = 10007, 64
+    re = torch.from_numpy(rng.standard_normal((b, n)).astype(np.float32))
+    im = torch.from_numpy(rng.standard_normal((b, n)).astype(np.float32))
+    if pinned:
+        re, im = re.pin_memory(), im.pin_memory()
+    out_r = torch.empty_like(re)
+    out_i = torch.empty_like(im)
+    for inverse in (False, True):
+        sf.fft_split(re, im, out=(out_r, out_i), inverse=inverse)
+        dr, di = sf.fft_split(re.cuda(), im.cuda(), inverse=inverse)
+        assert torch.equal(out_r, dr.cpu()) and torch.equal(out_i, di.cpu())
