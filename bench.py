@@ -175,12 +175,39 @@ def _cpu_worker(args):
     return time.perf_counter() - t0
 
 
+def _cpu_one_signal(args):
+    m, algorithm = args
+    sys.path.insert(0, ROOT)
+    from oracle import oracle
+    rng = np.random.default_rng(4)
+    re, im = rng.standard_normal(1 << m), rng.standard_normal(1 << m)
+    plan = oracle.NumpyPlan(m, algorithm)
+    t0 = time.perf_counter()
+    oracle.split_to_split_numpy(plan, re, im)
+    return time.perf_counter() - t0
+
+
+def cpu_port_rate_long(cfg, algorithm, sample_m=20):
+    """A single very long transform cannot be split across processes in the
+    reference (no internal parallelism): time the numpy port on one
+    2^sample_m-point signal and extrapolate by N log2 N."""
+    t = _cpu_one_signal((sample_m, algorithm))
+    scale = (cfg.n * cfg.log2n) / ((1 << sample_m) * sample_m)
+    per = t * scale
+    sample = (f"one 2^{sample_m}-point transform of the numpy port (transform.py:208-238) in "
+              f"{t:.3f} s, extrapolated to N=2^{cfg.log2n} by N*log2N ({per:.1f} s per transform); "
+              f"1 process (a single transform does not split)")
+    return 1.0 / per, 1, sample, per
+
+
 def cpu_port_rate(cfg, algorithm, target_s, procs=None):
     """Transforms/s of the numpy port of the reference executor over all host
     cores (one process per core, the reference has no internal parallelism).
     Sample: every worker transforms the first r rows of the config stream,
     with r sized so that one worker computes for about target_s seconds."""
     import multiprocessing as mp
+    if cfg.log2n > 16:
+        return cpu_port_rate_long(cfg, algorithm)
     procs = procs or os.cpu_count() or 1
     # size the sample with a 1-process probe
     probe_rows = max(1, min(cfg.batch, 64 if cfg.log2n <= 12 else 1))
@@ -215,6 +242,19 @@ def run_reference(args):
     if rank != 0:
         return
     procs = os.cpu_count() or 1
+    if cfg.log2n > 16:
+        rate, procs, sample, per = cpu_port_rate_long(cfg, args.algorithm)
+        line = {
+            "impl": "reference", "metric": BASELINE_METRIC, "value": rate, "unit": "transforms/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg.name, "n": cfg.n, "batch": cfg.batch},
+            "cpu_baseline": {"value": rate, "unit": "transforms/s", "cores": procs, "kind": "port",
+                             "sample": sample, "cpu_model": cpu_model()},
+            "e2e": {"value": rate, "unit": "transforms/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
     per_step_target = 1.0
     rate, procs, sample, per_row = cpu_port_rate(cfg, args.algorithm, min(2.0, per_step_target), procs)
     # steps: each a bounded sample (the same row prefix) on all cores
@@ -362,8 +402,11 @@ def run_ours(args):
         return
 
     peak, peak_src = peaks()
-    bytes_per_launch = 4 * n * cfg.elem_bytes * b / plan.launches_per_exec
-    achieved = 4 * n * cfg.elem_bytes * b / (kern_ms * plan.launches_per_exec / 1e3) / 1e9
+    # every launch reads and writes both planes of the whole batch once: the
+    # fused kernel is the whole transform, each pass-group launch of the
+    # multi-launch schedule (N > 4096) moves the same 4*N*sizeof(real) bytes
+    bytes_per_launch = 4 * n * cfg.elem_bytes * b
+    achieved = bytes_per_launch / (kern_ms / 1e3) / 1e9
     traffic = ncu_traffic(cfg.name)
     line = {
         "metric": BASELINE_METRIC,
@@ -388,6 +431,7 @@ def run_ours(args):
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": f"sfft_fused_kernel<{cfg.dtype},{cfg.log2n}>" if cfg.log2n <= 12 else "sfft_pass_kernel",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
+                     "launches_per_step": plan.launches_per_exec,
                      "kernel_ms": kern_ms, "peak_source": peak_src,
                      "frac_of_datasheet_8tbs": achieved / 8000.0},
         "gpu_launches": int(launches),
@@ -404,10 +448,91 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_sharded(args):
+    """Config 5 on N > 1 GPUs: one N = 2^28 transform, sharded four-step
+    (phase 0, all-to-all of both planes over NCCL, phase 1); strong scaling."""
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    from paper_2504_07264_b200 import _ffi
+    from paper_2504_07264_b200 import dist as sdist
+
+    cfg = workloads.CONFIGS[args.config]
+    dt = torch.float32 if cfg.dtype == "f32" else torch.float64
+    plan = sdist.DistPlan(cfg.log2n, world, rank, dtype=dt, device=device)
+    nl = plan.local_elems
+    g = torch.Generator(device=device).manual_seed(cfg.seed * 1000 + rank)
+    xr = torch.randn(nl, generator=g, device=device, dtype=torch.float64).to(dt)
+    xi = torch.randn(nl, generator=g, device=device, dtype=torch.float64).to(dt)
+    sr, si, rr, ri, yr, yi = (torch.empty_like(xr) for _ in range(6))
+    ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=device)
+
+    def step():
+        plan.phase(0, xr, xi, sr, si, workspace=ws)
+        dist.all_to_all_single(rr, sr)
+        dist.all_to_all_single(ri, si)
+        plan.phase(1, rr, ri, yr, yi, workspace=ws)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(device)
+    clocks = ClockSampler(device)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize(device)
+    l0 = _ffi.launch_count()
+    stream = torch.cuda.current_stream(device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(device)
+    t1 = time.perf_counter()
+    dist.barrier()
+    launches = _ffi.launch_count() - l0
+    clocks.mark(t0, t1)
+    clocks.stop()
+    ms_t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=device)
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    if rank == 0:
+        peak, src = peaks()
+        moved = 2 * len(plan_groups(cfg.log2n)) * 2 * nl * (4 if cfg.dtype == "f32" else 8)
+        line = {
+            "metric": BASELINE_METRIC, "value": 1.0 / (ms / 1e3), "unit": "transforms/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded per rank)",
+            "config": {"workload": cfg.name, "n": cfg.n, "batch": 1,
+                       "parallelism": f"sharded four-step x{world}, NCCL all-to-all of both planes"},
+            "gbs_algorithmic": 4 * cfg.n * (4 if cfg.dtype == "f32" else 8) / (ms / 1e3) / 1e9,
+            "roofline": {"bound": "hbm", "achieved": moved / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": moved / (ms / 1e3) / 1e9 / peak, "traffic": None,
+                         "note": "per-rank HBM bytes of all pass launches / step time (includes the all-to-all)",
+                         "peak_source": src},
+            "gpu_launches": int(launches), "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def plan_groups(m):
+    g = (m + 8) // 9
+    return [m // g + (1 if k < m % g else 0) for k in range(g)]
+
+
 def main():
     args = parse()
+    world, _, _ = dist_env()
     if args.impl == "reference":
         run_reference(args)
+    elif world > 1 and workloads.CONFIGS[args.config].batch == 1:
+        run_sharded(args)
     else:
         run_ours(args)
 
