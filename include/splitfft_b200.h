@@ -77,7 +77,11 @@ int sfft_plan_create(int log2n, int dtype, int algorithm, int device,
                      int max_log2n, sfft_plan **out);
 
 /* Same, with an explicit register radix (log2; 0 = tuned default) and
- * kernel family (SFFT_KERNEL_*).  Used by the tuner and the tests. */
+ * kernel family (SFFT_KERNEL_*), optionally OR-ed with SFFT_PRE_OFF /
+ * SFFT_PRE_ON (fp32: fetch each pass's base factors before the data; the
+ * default follows the tuned table).  Used by the tuner and the tests. */
+#define SFFT_PRE_OFF 0x10
+#define SFFT_PRE_ON 0x20
 int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device,
                         int max_log2n, int log2_radix, int kernel,
                         sfft_plan **out);

@@ -131,6 +131,7 @@ struct sfft_plan {
     int kernel = SFFT_KERNEL_AUTO;  // fused-path kernel family
     int lr_tma = -1;                // radix of the TMA kernel (-1: none)
     int lr_ldg_il = 0;              // radix of the interleaved LDG kernel
+    bool pre = false;               // fp32: fetch pass base factors up front
     // fused path
     void *d_tw = nullptr;          // stage-major vec2_t<T> table, stages 1..cat_top
     int cat_top = 0;
@@ -268,7 +269,7 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
                              ((size_t)is * esz) % 16 == 0 && ((size_t)os * esz) % 16 == 0 &&
                              batch < (int64_t(1) << 31);
         if (!il && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG && aligned) {
-            TmaLaunchFn tf = tma_launcher(p->dtype, m, p->lr_tma, p->algo == SFFT_DIF);
+            TmaLaunchFn tf = tma_launcher(p->dtype, m, p->lr_tma, p->algo == SFFT_DIF, p->pre);
             if (tf) {
                 TmaLaunch L;
                 L.x_re = x0;
@@ -290,7 +291,7 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
             return fail(SFFT_EINVAL, "the TMA kernel needs planar, 16-byte aligned rows with 16-byte row strides "
                                      "and a size with a TMA configuration (log2n=%d)", m);
         const int lr = il ? p->lr_ldg_il : p->lr;
-        FusedLaunchFn fn = fused_launcher_algo(p->dtype, m, lr, p->algo == SFFT_DIF, il);
+        FusedLaunchFn fn = fused_launcher_algo(p->dtype, m, lr, p->algo == SFFT_DIF, il, !il && p->pre);
         if (!fn) return fail(SFFT_EINVAL, "no fused kernel for log2n=%d radix=2^%d layout=%s", m, lr,
                              il ? "interleaved" : "planar");
         FusedArgs a;
@@ -415,7 +416,9 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
     if (algorithm != SFFT_DIT && algorithm != SFFT_DIF)
         return fail(SFFT_EINVAL, "%d is not a valid Algorithm (0 = dit, 1 = dif)", algorithm);
     if (dtype != SFFT_F32 && dtype != SFFT_F64) return fail(SFFT_EINVAL, "unknown dtype %d", dtype);
-    if (kernel != SFFT_KERNEL_AUTO && kernel != SFFT_KERNEL_LDG && kernel != SFFT_KERNEL_TMA)
+    const int pre_pref = (kernel >> 4) & 3;   // 0 auto, 1 off, 2 on
+    kernel &= 0xf;
+    if ((kernel != SFFT_KERNEL_AUTO && kernel != SFFT_KERNEL_LDG && kernel != SFFT_KERNEL_TMA) || pre_pref == 3)
         return fail(SFFT_EINVAL, "unknown kernel family %d", kernel);
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -435,9 +438,10 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
     int rc = SFFT_OK;
     p->kernel = kernel;
     if (log2n <= kFusedMaxLog) {
-        bool auto_tma = false;
+        bool auto_tma = false, auto_pre = false;
         int auto_lr = 0;
-        auto_choice(dtype, log2n, &auto_tma, &auto_lr);
+        auto_choice(dtype, log2n, &auto_tma, &auto_lr, &auto_pre);
+        p->pre = pre_pref == 2 || (pre_pref == 0 && kernel == SFFT_KERNEL_AUTO && log2_radix <= 0 && auto_pre);
         int lr;
         if (log2_radix > 0) lr = log2_radix;
         else if (kernel == SFFT_KERNEL_AUTO) lr = auto_lr;
@@ -453,7 +457,7 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
         p->lr_ldg_il = fused_default_lr(dtype, log2n);
         const bool want_tma = kernel == SFFT_KERNEL_TMA ||
                               (kernel == SFFT_KERNEL_AUTO && (log2_radix > 0 || auto_tma));
-        if (want_tma && tma_launcher(dtype, log2n, lr, false)) p->lr_tma = lr;
+        if (want_tma && tma_launcher(dtype, log2n, lr, false, p->pre)) p->lr_tma = lr;
         if (kernel == SFFT_KERNEL_TMA && p->lr_tma < 0) {
             delete p;
             return fail(SFFT_EINVAL, "no TMA kernel for log2n=%d radix=2^%d", log2n, lr);

@@ -166,6 +166,18 @@ template <> struct SmallTw<double> {
 template <typename T> struct FactorTw { static constexpr bool value = false; };
 template <> struct FactorTw<float> { static constexpr bool value = true; };
 
+// Per-stage base factors w_{gs+t}(cbase), t = 1..K, of one virtual thread
+// (fp32 factored twiddles).  Kernels call this once, ahead of the data (and
+// for persistent kernels once for all tiles), and pass the array to
+// dit_stages/dif_stages as `pre`, so no table or two-level lookup sits on
+// the critical path of a pass.
+template <typename T, int K, typename TW>
+__device__ __forceinline__ void load_bases(vec2_t<T> *pre, int gs, typename TW::index_t cbase, const TW &tw)
+{
+#pragma unroll
+    for (int t = 1; t <= K; ++t) pre[t - 1] = tw.get(gs + t, cbase);
+}
+
 // K consecutive DIT stages (global stages gs+1 .. gs+K) on the 2^K values
 // v[0..2^K) of one virtual thread.  Register position p holds, before stage
 // t, the (size 2^(gs+t-1)) partial transform of sub-sequence (p mod
@@ -177,7 +189,8 @@ template <> struct FactorTw<float> { static constexpr bool value = true; };
 // TRIV = false promises gs >= 1 and no trivial factors to skip (every pass
 // group after the first), which removes the per-stage kind tests.
 template <typename T, int K, bool TRIV = true, typename TW>
-__device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw)
+__device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw,
+                                           const vec2_t<T> *pre = nullptr)
 {
     using I = typename TW::index_t;
     const bool first = TRIV && gs == 0;   // first pass: every factor is a compile-time constant
@@ -186,7 +199,7 @@ __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::in
         const int half = (1 << K) >> t;
         const int i = gs + t;
         vec2_t<T> base;
-        if (!first && FactorTw<T>::value) base = tw.get(i, cbase);
+        if (!first && FactorTw<T>::value) base = pre ? pre[t - 1] : tw.get(i, cbase);
 #pragma unroll
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;
@@ -235,7 +248,8 @@ __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::in
 // Transpose of dit_stages: DIF stages gs+K .. gs+1 (descending), same
 // register map run backwards.
 template <typename T, int K, bool TRIV = true, typename TW>
-__device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw)
+__device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw,
+                                           const vec2_t<T> *pre = nullptr)
 {
     using I = typename TW::index_t;
     const bool first = TRIV && gs == 0;
@@ -244,7 +258,7 @@ __device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, typename TW::in
         const int half = (1 << K) >> t;
         const int i = gs + t;
         vec2_t<T> base;
-        if (!first && FactorTw<T>::value) base = tw.get(i, cbase);
+        if (!first && FactorTw<T>::value) base = pre ? pre[t - 1] : tw.get(i, cbase);
 #pragma unroll
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;

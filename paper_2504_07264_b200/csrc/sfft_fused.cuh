@@ -121,7 +121,7 @@ __device__ __forceinline__ void sig_sync()
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool valid,
                                          T *sr, T *si, const GIO<T, IL> &io,
-                                         const TwCat<T> &tw)
+                                         const TwCat<T> &tw, const vec2_t<T> *pre)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
     constexpr int N = Sh::N, R = Sh::R, P = Sh::P, LR = Sh::LR;
@@ -150,7 +150,8 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = t + P * u;
-        dit_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (j & (NS - 1)), tw);
+        dit_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (j & (NS - 1)), tw,
+                          (pre && p > 0) ? pre + p * R + u * KP : nullptr);
     }
     // scatter in Stockham order
     if constexpr (!LAST) {
@@ -182,11 +183,12 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dit_from(T *vr, T *vi, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw)
+                                         T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw,
+                                         const vec2_t<T> *pre)
 {
     if constexpr (p < FusedShape<LOGN, LR_REQ>::NPASS) {
-        dit_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw);
-        dit_from<T, LOGN, LR_REQ, IL, p + 1>(vr, vi, t, row, valid, sr, si, io, tw);
+        dit_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw, pre);
+        dit_from<T, LOGN, LR_REQ, IL, p + 1>(vr, vi, t, row, valid, sr, si, io, tw, pre);
     }
 }
 
@@ -194,7 +196,7 @@ __device__ __forceinline__ void dit_from(T *vr, T *vi, int t, int64_t row, bool 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool valid,
                                          T *sr, T *si, const GIO<T, IL> &io,
-                                         const TwCat<T> &tw)
+                                         const TwCat<T> &tw, const vec2_t<T> *pre)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
     constexpr int N = Sh::N, R = Sh::R, P = Sh::P, LR = Sh::LR;
@@ -223,7 +225,8 @@ __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = t + P * u;
-        dif_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (j & (NS - 1)), tw);
+        dif_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (j & (NS - 1)), tw,
+                          (pre && p > 0) ? pre + p * R + u * KP : nullptr);
     }
     if constexpr (!LAST) {
         if constexpr (!FIRST) sig_sync<P>();
@@ -253,15 +256,19 @@ __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool 
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dif_from(T *vr, T *vi, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw)
+                                         T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw,
+                                         const vec2_t<T> *pre)
 {
     if constexpr (p >= 0) {
-        dif_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw);
-        dif_from<T, LOGN, LR_REQ, IL, p - 1>(vr, vi, t, row, valid, sr, si, io, tw);
+        dif_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw, pre);
+        dif_from<T, LOGN, LR_REQ, IL, p - 1>(vr, vi, t, row, valid, sr, si, io, tw, pre);
     }
 }
 
-template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL>
+// PRE (fp32 only): fetch the base factors of passes >= 1 before the data.
+// Whether that pays depends on the size (register pressure vs latency);
+// tools/tune.py measures both and gen_inst.py's AUTO table records the pick.
+template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL, bool PRE = false>
 __global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT)
 sfft_fused_kernel(const FusedArgs a)
 {
@@ -287,10 +294,28 @@ sfft_fused_kernel(const FusedArgs a)
         T vr[R], vi[R];
         T *sr = sbase + sl * SSTR;
         T *si = sbase + S * SSTR + sl * SSTR;
+        // fp32: the base factors of passes >= 1, fetched before any data
+        vec2_t<T> pre[Sh::NPASS * R];
+        if constexpr (PRE && FactorTw<T>::value) {
+#pragma unroll
+            for (int p = 1; p < Sh::NPASS; ++p) {
+                const int sp = p * Sh::LR;
+                const int kp = cmin(Sh::LR, LOGN - sp);
+#pragma unroll
+                for (int u = 0; u < R / (1 << kp); ++u) {
+                    const int j = t + P * u;
+#pragma unroll
+                    for (int tt = 1; tt <= kp; ++tt)
+                        pre[p * R + u * kp + tt - 1] = tw.get(sp + tt, j & ((1 << sp) - 1));
+                }
+            }
+        }
         if constexpr (DIF)
-            dif_from<T, LOGN, LR_REQ, IL, Sh::NPASS - 1>(vr, vi, t, row, valid, sr, si, io, tw);
+            dif_from<T, LOGN, LR_REQ, IL, Sh::NPASS - 1>(vr, vi, t, row, valid, sr, si, io, tw,
+                                                         (PRE && FactorTw<T>::value) ? pre : nullptr);
         else
-            dit_from<T, LOGN, LR_REQ, IL, 0>(vr, vi, t, row, valid, sr, si, io, tw);
+            dit_from<T, LOGN, LR_REQ, IL, 0>(vr, vi, t, row, valid, sr, si, io, tw,
+                                             (PRE && FactorTw<T>::value) ? pre : nullptr);
     }
 }
 

@@ -27,7 +27,7 @@ constexpr int kPassMinL = 4, kPassMaxL = 9;
 // dtype: 0 = f32, 1 = f64.  Interleaved variants exist only for the
 // default radix of each size.  The returned fused launcher is bound to
 // (dif, il) already and ignores those two arguments.
-FusedLaunchFn fused_launcher_algo(int dtype, int logn, int lr, bool dif, bool il);
+FusedLaunchFn fused_launcher_algo(int dtype, int logn, int lr, bool dif, bool il, bool pre = false);
 int fused_default_lr(int dtype, int logn);
 PassLaunchFn pass_launcher(int dtype, int L);
 int pass_tile(int dtype);           // TJ: sub-problems per CTA
@@ -35,11 +35,11 @@ int pass_default_lr(int dtype);
 PassLaunchFn pass_launcher_f32(int L);
 PassLaunchFn pass_launcher_f64(int L);
 
-TmaLaunchFn tma_launcher(int dtype, int logn, int lr, bool dif);
-TmaLaunchFn tma_launcher_f32(int logn, int lr, bool dif);
-TmaLaunchFn tma_launcher_f64(int logn, int lr, bool dif);
+TmaLaunchFn tma_launcher(int dtype, int logn, int lr, bool dif, bool pre = false);
+TmaLaunchFn tma_launcher_f32(int logn, int lr, bool dif, bool pre);
+TmaLaunchFn tma_launcher_f64(int logn, int lr, bool dif, bool pre);
 int tma_default_lr(int dtype, int logn);   // -1: no TMA config for this size
-void auto_choice(int dtype, int logn, bool *tma, int *lr);  // kernel=auto pick, 0 <= logn <= 12
+void auto_choice(int dtype, int logn, bool *tma, int *lr, bool *pre);  // kernel=auto pick, 0 <= logn <= 12
 
 void count_launch();
 

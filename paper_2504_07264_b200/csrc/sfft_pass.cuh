@@ -216,6 +216,32 @@ sfft_pass_kernel(const PassArgs a)
 
     T vr[R], vi[R];
 
+    // fp32 groups after the first: every base factor of every internal pass,
+    // fetched up front (independent of the data) -- pre[pass][u*K + t-1]
+    // (measured: fetching them up front raises register use 63 -> 79 and
+    // costs ~6% on N = 2^28, tools/ab_cfg5.sh; enable with -DSFFT_PASS_PRE)
+#ifdef SFFT_PASS_PRE
+    constexpr bool PRE = FactorTw<T>::value && !S0;
+#else
+    constexpr bool PRE = false;
+#endif
+    vec2_t<T> pre[NPI][R];
+    if constexpr (PRE) {
+#pragma unroll
+        for (int pp = 0; pp < NPI; ++pp) {
+            const int sp = pp * LR;
+            const int kp = cmin(LR, L - sp);
+            const int nsp = 1 << sp;
+#pragma unroll
+            for (int u = 0; u < R / (1 << kp); ++u) {
+                const int jp = t + P * u;
+                const I cb = (I)(c + ((uint32_t)(jp & (nsp - 1)) << S));
+#pragma unroll
+                for (int tt = 1; tt <= kp; ++tt) pre[pp][u * kp + tt - 1] = tw.get(S + sp + tt, cb);
+            }
+        }
+    }
+
     if constexpr (!DIF) {
         // ------------------------------ DIT ------------------------------
 #pragma unroll
@@ -243,7 +269,8 @@ sfft_pass_kernel(const PassArgs a)
         {                                                                                       \
             const int jp = t + P * u;                                                           \
             dit_stages<T, KP, S0>(vr + u * RP, vi + u * RP, S + sp,                             \
-                                  (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw);              \
+                                  (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw,               \
+                                  PRE ? &pre[pp][u * KP] : nullptr);                            \
         }                                                                                       \
         const bool last = pp == NPI - 1;                                                        \
         if (!last || S0) {                                                                      \
@@ -331,7 +358,8 @@ sfft_pass_kernel(const PassArgs a)
         {                                                                                       \
             const int jp = t + P * u;                                                           \
             dif_stages<T, KP, S0>(vr + u * RP, vi + u * RP, S + sp,                             \
-                                  (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw);              \
+                                  (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw,               \
+                                  PRE ? &pre[pp][u * KP] : nullptr);                            \
         }                                                                                       \
         if (pp != 0) {                                                                          \
             if (!first || S0) __syncthreads();                                                  \

@@ -135,7 +135,7 @@ __device__ __forceinline__ void sts_at(unsigned char *base, uint32_t off, T v)
     *reinterpret_cast<T *>(base + off) = v;
 }
 
-template <typename T, int LOGN, int LR_REQ, bool DIF, int NT_REQ, int STAGES, int OB>
+template <typename T, int LOGN, int LR_REQ, bool DIF, int NT_REQ, int STAGES, int OB, bool PRE_T = false>
 __global__ void __launch_bounds__(TmaShape<T, LOGN, LR_REQ, NT_REQ, STAGES, OB>::NT)
 sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant__ CUtensorMap in_im,
                 const __grid_constant__ CUtensorMap out_re, const __grid_constant__ CUtensorMap out_im,
@@ -178,6 +178,23 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
     }
 
     T vr[R], vi[R];
+    // fp32: base factors of passes >= 1 depend only on the thread, not on
+    // the tile -- fetch them once for the whole persistent loop
+    constexpr bool PRE = PRE_T && FactorTw<T>::value;
+    vec2_t<T> pre[NPASS][R];
+    if constexpr (PRE) {
+#pragma unroll
+        for (int p = 1; p < NPASS; ++p) {
+            const int sp = p * LR;
+            const int kp = cmin(LR, LOGN - sp);
+#pragma unroll
+            for (int u = 0; u < R / (1 << kp); ++u) {
+                const int j = t + P * u;
+#pragma unroll
+                for (int tt = 1; tt <= kp; ++tt) pre[p][u * kp + tt - 1] = tw.get(sp + tt, j & ((1 << sp) - 1));
+            }
+        }
+    }
     T *exr = ex + sl * SSTR;
     T *exi = ex + S * SSTR + sl * SSTR;
 
@@ -219,7 +236,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
         {                                                                                            \
             const int j = t + P * u;                                                                 \
-            dit_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (j & (ns - 1)), tw);            \
+            dit_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (j & (ns - 1)), tw,              \
+                              (PRE && p > 0) ? &pre[p][u * KP] : nullptr);                       \
         }                                                                                            \
         if (p < NPASS - 1) {                                                                         \
             if (p > 0) __syncthreads();                                                              \
@@ -300,7 +318,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
         {                                                                                            \
             const int j = t + P * u;                                                                 \
-            dif_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (j & (ns - 1)), tw);            \
+            dif_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (j & (ns - 1)), tw,              \
+                              (PRE && p > 0) ? &pre[p][u * KP] : nullptr);                       \
         }                                                                                            \
         if (p > 0) {                                                                                 \
             if (q > 0) __syncthreads();                                                              \

@@ -42,11 +42,11 @@ inline cudaError_t encode_plane(CUtensorMap *map, const void *ptr, int n, int64_
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <typename T, int LOGN, int LR, bool DIF, int NT_REQ, int STAGES, int OB>
+template <typename T, int LOGN, int LR, bool DIF, int NT_REQ, int STAGES, int OB, bool PRE>
 cudaError_t launch_tma(const TmaLaunch &L, cudaStream_t st)
 {
     using Sh = TmaShape<T, LOGN, LR, NT_REQ, STAGES, OB>;
-    auto k = sfft_tma_kernel<T, LOGN, LR, DIF, NT_REQ, STAGES, OB>;
+    auto k = sfft_tma_kernel<T, LOGN, LR, DIF, NT_REQ, STAGES, OB, PRE>;
     static int blocks_per_sm[32] = {0};
     static int num_sms[32] = {0};
     int dev = 0;

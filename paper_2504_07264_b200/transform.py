@@ -142,7 +142,8 @@ class FftPlan:
 
 
 def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
-              dtype=torch.float64, device=None, radix_log: int = 0, kernel: str = "auto") -> FftPlan:
+              dtype=torch.float64, device=None, radix_log: int = 0, kernel: str = "auto",
+              prefetch_factors=None) -> FftPlan:
     """Build an FftPlan for 2**m samples on a CUDA device (transform.py:65-85).
 
     Same validation order and messages as the reference: m < 0 -> ValueError,
@@ -150,7 +151,9 @@ def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
     the plane dtype (float64 like the reference, or float32); ``radix_log``
     overrides the register radix of the fused kernel (0 = tuned default);
     ``kernel`` picks the fused kernel family: "auto" (TMA-fed when the rows
-    allow it), "ldg" (per-thread loads) or "tma" (required).
+    allow it), "ldg" (per-thread loads) or "tma" (required);
+    ``prefetch_factors`` (fp32) forces fetching each pass's base factors
+    before the data on/off (None = tuned default).
     """
     if m < 0:
         raise ValueError(f"stage count m must be >= 0, got {m}")
@@ -163,11 +166,12 @@ def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
     kernels = {"auto": _ffi.SFFT_KERNEL_AUTO, "ldg": _ffi.SFFT_KERNEL_LDG, "tma": _ffi.SFFT_KERNEL_TMA}
     if kernel not in kernels:
         raise ValueError(f"kernel must be one of {sorted(kernels)}, got {kernel!r}")
+    kcode = kernels[kernel] | {None: 0, False: 0x10, True: 0x20}[prefetch_factors]
     handle = ctypes.c_void_p()
     algo = _ffi.SFFT_DIF if algorithm is Algorithm.DIF else _ffi.SFFT_DIT
     _ffi.check(_ffi.lib.sfft_plan_create_ex(int(m), _DTYPE_CODE[dtype], algo, device.index,
                                             int(min(max_m, MAX_PLAN_M)),
-                                            int(radix_log), kernels[kernel], ctypes.byref(handle)))
+                                            int(radix_log), kcode, ctypes.byref(handle)))
     return FftPlan(m, algorithm, dtype, device, handle.value)
 
 

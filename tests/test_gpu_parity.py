@@ -34,10 +34,11 @@ def rand(rng, b, n, dtype):
     return re, im
 
 
-def gpu_split(re, im, algo="dit", inverse=False, radix_log=0):
+def gpu_split(re, im, algo="dit", inverse=False, radix_log=0, kernel="auto", prefetch=None):
     dt = torch.float32 if re.dtype == np.float32 else torch.float64
     m = re.shape[-1].bit_length() - 1
-    plan = sf.make_plan(m, algo, dtype=dt, device="cuda:0", radix_log=radix_log)
+    plan = sf.make_plan(m, algo, dtype=dt, device="cuda:0", radix_log=radix_log, kernel=kernel,
+                        prefetch_factors=prefetch)
     xr = torch.from_numpy(re).cuda()
     xi = torch.from_numpy(im).cuda()
     yr, yi = sf.fft_split(xr, xi, inverse=inverse, plan=plan)
@@ -75,16 +76,19 @@ def test_f32_rel_l2_vs_oracle(cuda, m, algo, inverse):
     assert err <= F32_TOL(m), f"relL2 {err:.3e} > {F32_TOL(m):.1e}"
 
 
+@pytest.mark.parametrize("prefetch", [False, True])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("algo", ["dit", "dif"])
 @pytest.mark.parametrize("m,lr", [(m, lr) for m in (4, 5, 6, 7, 9, 10, 11, 12) for lr in (2, 3, 4, 5)
                                   if (1 << (m - min(lr, m))) <= 1024])
-def test_every_radix_schedule(cuda, m, lr, algo, dtype):
+def test_every_radix_schedule(cuda, m, lr, algo, dtype, prefetch):
     if dtype == np.float64 and lr == 5:
         pytest.skip("fp64 register radix is capped at 2^4")
+    if dtype == np.float64 and prefetch:
+        pytest.skip("fp64 reads every factor from the table")
     rng = np.random.default_rng(3000 + 16 * m + lr)
     re, im = rand(rng, 19, 1 << m, dtype)
-    gr, gi = gpu_split(re, im, algo, False, radix_log=lr)
+    gr, gi = gpu_split(re, im, algo, False, radix_log=lr, kernel="ldg", prefetch=prefetch)
     wr, wi = oracle.fft_split_c(re, im, algo, False)
     if dtype == np.float64:
         assert np.array_equal(bits(gr), bits(wr)) and np.array_equal(bits(gi), bits(wi))
@@ -194,9 +198,12 @@ TMA_CASES = [("f32", m, lr) for m, lrs in {5: [3], 6: [3, 2], 7: [3, 4], 8: [3, 
                                             10: [3, 4], 11: [4]}.items() for lr in lrs]
 
 
+@pytest.mark.parametrize("prefetch", [False, True])
 @pytest.mark.parametrize("algo", ["dit", "dif"])
 @pytest.mark.parametrize("dt,m,lr", TMA_CASES)
-def test_tma_kernel_many_tiles(cuda, dt, m, lr, algo):
+def test_tma_kernel_many_tiles(cuda, dt, m, lr, algo, prefetch):
+    if dt == "f64" and prefetch:
+        pytest.skip("fp64 reads every factor from the table")
     # enough rows for several tiles per persistent CTA (stage and output-buffer
     # reuse) plus a ragged tail tile
     dtype = np.float32 if dt == "f32" else np.float64
@@ -204,7 +211,8 @@ def test_tma_kernel_many_tiles(cuda, dt, m, lr, algo):
     b = (1 << 22 >> m) + 3
     rng = np.random.default_rng(7000 + m + 31 * lr)
     re, im = rand(rng, b, 1 << m, dtype)
-    plan = sf.make_plan(m, algo, dtype=tdt, device="cuda:0", radix_log=lr, kernel="tma")
+    plan = sf.make_plan(m, algo, dtype=tdt, device="cuda:0", radix_log=lr, kernel="tma",
+                        prefetch_factors=prefetch)
     assert plan.kernel == "tma"
     xr, xi = torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda()
     for inverse in (False, True):
@@ -216,7 +224,8 @@ def test_tma_kernel_many_tiles(cuda, dt, m, lr, algo):
         else:
             assert rel_l2(gr.astype(np.float64), gi.astype(np.float64), wr, wi) <= F32_TOL(m)
             # and bit-identical to the LDG kernel (same arithmetic, other data path)
-            ldg = sf.make_plan(m, algo, dtype=tdt, device="cuda:0", radix_log=lr, kernel="ldg")
+            ldg = sf.make_plan(m, algo, dtype=tdt, device="cuda:0", radix_log=lr, kernel="ldg",
+                               prefetch_factors=prefetch)
             lr_, li_ = sf.fft_split(xr, xi, plan=ldg, inverse=inverse)
             assert torch.equal(lr_, yr) and torch.equal(li_, yi)
 
