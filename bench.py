@@ -402,6 +402,8 @@ def run_ours(args):
         return
 
     peak, peak_src = peaks()
+    import dataclasses
+    census = dataclasses.asdict(sf.count_flops(cfg.log2n))
     # every launch reads and writes both planes of the whole batch once: the
     # fused kernel is the whole transform, each pass-group launch of the
     # multi-launch schedule (N > 4096) moves the same 4*N*sizeof(real) bytes
@@ -427,9 +429,13 @@ def run_ours(args):
                    "l2": f"inputs {2 * n * cfg.elem_bytes * b / 2**20:.0f} MiB > 126 MB L2 (no flush needed)"},
         "gbs_algorithmic": 4 * n * cfg.elem_bytes * b * world / (ms / 1e3) / 1e9,
         "gflops_5nlogn": 5 * n * cfg.log2n * b * world / (ms / 1e3) / 1e9,
+        # the reference's own census (count_flops, transform.py:312-335) next to 5N log2N
+        "census": census,
+        "gflops_census": (census["real_mults"] + census["real_adds"]) * b * world / (ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
-                     "kernel": f"sfft_fused_kernel<{cfg.dtype},{cfg.log2n}>" if cfg.log2n <= 12 else "sfft_pass_kernel",
+                     "kernel": {"tma": "sfft_tma_kernel", "ldg": "sfft_fused_kernel",
+                                "pass": "sfft_pass_kernel"}[plan.kernel] + f"<{cfg.dtype}, log2N={cfg.log2n}>",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "launches_per_step": plan.launches_per_exec,
                      "kernel_ms": kern_ms, "peak_source": peak_src,
