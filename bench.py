@@ -40,6 +40,7 @@ import workloads  # noqa: E402
 
 BASELINE_METRIC = "batched split-DFT transforms/s and achieved HBM GB/s vs peak at 1/2/4/8 B200"
 FALLBACK_HBM_GBS = 6650.0
+SPINUP_S = 0.3   # extra untimed warm-up time after the W warm-up steps (clock ramp)
 
 
 def parse():
@@ -328,6 +329,13 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(device)
+    # the W warm-up steps of a 0.2 ms step leave an idle GPU at low clocks;
+    # keep stepping (untimed) until the clocks have ramped (>= SPINUP_S)
+    spin0 = time.perf_counter()
+    while time.perf_counter() - spin0 < SPINUP_S:
+        for _ in range(20):
+            step()
+        torch.cuda.synchronize(device)
 
     clocks = ClockSampler(device)
     clocks.start()
@@ -426,7 +434,8 @@ def run_ours(args):
         "config": {"workload": cfg.name, "n": n, "batch_per_gpu": b, "global_batch": b * world,
                    "input_dtype": cfg.dtype, "seed": cfg.seed, "algorithm": args.algorithm,
                    "radix_log": plan.radix_log, "parallelism": f"batch-sharded x{world}, no collective",
-                   "l2": f"inputs {2 * n * cfg.elem_bytes * b / 2**20:.0f} MiB > 126 MB L2 (no flush needed)"},
+                   "l2": f"inputs {2 * n * cfg.elem_bytes * b / 2**20:.0f} MiB > 126 MB L2 (no flush needed)",
+                   "extra_warmup_s": SPINUP_S},
         "gbs_algorithmic": 4 * n * cfg.elem_bytes * b * world / (ms / 1e3) / 1e9,
         "gflops_5nlogn": 5 * n * cfg.log2n * b * world / (ms / 1e3) / 1e9,
         # the reference's own census (count_flops, transform.py:312-335) next to 5N log2N

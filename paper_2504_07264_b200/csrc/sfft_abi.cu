@@ -9,6 +9,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -222,9 +223,21 @@ void free_plan(sfft_plan *p)
     delete p;
 }
 
+// Largest group (log2 sub-problem size) of the multi-launch schedule.
+// 8 measured best for fp32 N = 2^28 (4 groups of 7 beat 3 groups of 9-10:
+// the 2^9/2^10-point groups fit one CTA per SM); SFFT_PASS_MAX_L overrides
+// (developer knob for tools/tune_large.py).
+static int pass_max_l()
+{
+    const char *e = getenv("SFFT_PASS_MAX_L");
+    int v = e ? atoi(e) : 8;
+    return v < kPassMinL ? kPassMinL : (v > kPassMaxL ? kPassMaxL : v);
+}
+
 std::vector<Group> split_groups(int m)
 {
-    const int G = (m + kPassMaxL - 1) / kPassMaxL;
+    const int maxl = pass_max_l();
+    const int G = (m + maxl - 1) / maxl;
     std::vector<Group> g;
     int S = 0;
     for (int k = 0; k < G; ++k) {
@@ -319,9 +332,9 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     const size_t plane = (size_t)batch * (size_t)n * esz;
     void *bufA[2] = {ws, ws + plane};
     void *bufB[2] = {ws + 2 * plane, ws + 3 * plane};
-    const int TJ = pass_tile(p->dtype);
     for (int k = 0; k < G; ++k) {
         const Group gr = p->algo == SFFT_DIF ? p->groups[G - 1 - k] : p->groups[k];
+        const int TJ = pass_tile(p->dtype, gr.L);
         PassLaunchFn fn = pass_launcher(p->dtype, gr.L);
         if (!fn) return fail(SFFT_EINVAL, "no pass kernel for L=%d", gr.L);
         PassArgs a;
@@ -470,7 +483,9 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
             rc = upload_table<float>(p, kFusedMaxLog, false);
             if (rc == SFFT_OK) rc = upload_two_level(p);
         } else {
-            rc = upload_table<double>(p, log2n < 20 ? log2n : 20, log2n > 20);
+            // fp64 keeps every stage in the stage-major table (bit-exact factors,
+            // coalesced reads; 2^m - 1 entries = 4 GiB at m = 28)
+            rc = upload_table<double>(p, log2n, false);
         }
     }
     if (rc != SFFT_OK) {
@@ -548,7 +563,8 @@ struct sfft_dist_plan {
 
 static std::vector<Group> split_range(int S0, int L)
 {
-    const int G = (L + kPassMaxL - 1) / kPassMaxL;
+    const int maxl = pass_max_l();
+    const int G = (L + maxl - 1) / maxl;
     std::vector<Group> g;
     int S = S0;
     for (int k = 0; k < G; ++k) {
@@ -640,10 +656,10 @@ int sfft_dist_exec_phase(const sfft_dist_plan *d, int phase, const void *x_re, c
     void *bufA[2] = {ws, ws + nl * esz};
     void *bufB[2] = {ws + 2 * nl * esz, ws + 3 * nl * esz};
     const bool inv = direction == SFFT_INVERSE;
-    const int TJ = pass_tile(p->dtype);
     const int G = (int)gs.size();
     for (int k = 0; k < G; ++k) {
         const Group gr = gs[k];
+        const int TJ = pass_tile(p->dtype, gr.L);
         PassLaunchFn fn = pass_launcher(p->dtype, gr.L);
         if (!fn) return fail(SFFT_EINVAL, "no pass kernel for L=%d", gr.L);
         PassArgs a;

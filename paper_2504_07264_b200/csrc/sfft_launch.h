@@ -21,7 +21,7 @@ using TmaLaunchFn = cudaError_t (*)(const TmaLaunch &L, cudaStream_t st);
 
 constexpr int kFusedMaxLog = 12;
 constexpr int kMaxRadixLog = 5;
-constexpr int kPassMinL = 4, kPassMaxL = 9;
+constexpr int kPassMinL = 4, kPassMaxL = 10;
 
 // Registry lookups (nullptr when the combination was not instantiated).
 // dtype: 0 = f32, 1 = f64.  Interleaved variants exist only for the
@@ -30,7 +30,7 @@ constexpr int kPassMinL = 4, kPassMaxL = 9;
 FusedLaunchFn fused_launcher_algo(int dtype, int logn, int lr, bool dif, bool il, bool pre = false);
 int fused_default_lr(int dtype, int logn);
 PassLaunchFn pass_launcher(int dtype, int L);
-int pass_tile(int dtype);           // TJ: sub-problems per CTA
+int pass_tile(int dtype, int L);    // TJ: sub-problems per CTA of a 2^L-point group
 int pass_default_lr(int dtype);
 PassLaunchFn pass_launcher_f32(int L);
 PassLaunchFn pass_launcher_f64(int L);
