@@ -15,6 +15,7 @@
 #include <atomic>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/splitfft_b200.h"
@@ -22,6 +23,7 @@
 #include "sfft_launch.h"
 #include "sfft_pass.cuh"
 #include "sfft_tma_host.h"
+#include "sfft_pass_tma_host.h"
 
 #include <mutex>
 
@@ -234,6 +236,16 @@ static int pass_max_l()
     return v < kPassMinL ? kPassMinL : (v > kPassMaxL ? kPassMaxL : v);
 }
 
+// The TMA-pipelined pass kernel (sfft_pass_tma.cuh) is correct (parity tests
+// run it with SFFT_PASS_TMA=1) but measured slower than the LDG pass kernel
+// (N = 2^28 fp32: 6.25 vs 3.83 ms -- twiddle latency with 8-16 warps per SM),
+// so it is opt-in until it is pipelined further.
+static bool pass_tma_enabled()
+{
+    const char *e = getenv("SFFT_PASS_TMA");
+    return e && atoi(e) != 0;
+}
+
 std::vector<Group> split_groups(int m)
 {
     const int maxl = pass_max_l();
@@ -374,6 +386,40 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         a.fine = p->d_fine;
         a.jb = 0;
         a.in_map.b = a.out_map.b = 0;
+        // groups after the first stage block: TMA-pipelined kernel when the
+        // planes are 16-byte aligned with 16-byte row strides
+        const bool planar_here = !((first || last) && il);
+        const bool al = (((uintptr_t)a.x0 | (uintptr_t)a.x1 | (uintptr_t)a.y0 | (uintptr_t)a.y1) % 16 == 0) &&
+                        ((size_t)a.in_stride * esz) % 16 == 0 && ((size_t)a.out_stride * esz) % 16 == 0 &&
+                        batch < (int64_t(1) << 31);
+        PassTmaLaunchFn tf = (pass_tma_enabled() && gr.S > 0 && planar_here && al && p->kernel != SFFT_KERNEL_LDG)
+                                 ? pass_tma_launcher(p->dtype, gr.L, p->algo == SFFT_DIF) : nullptr;
+        if (tf) {
+            PassTmaLaunch Lc;
+            Lc.x_re = a.x0;
+            Lc.x_im = a.x1;
+            Lc.y_re = a.y0;
+            Lc.y_im = a.y1;
+            Lc.batch = batch;
+            Lc.in_stride = a.in_stride;
+            Lc.out_stride = a.out_stride;
+            if (a.swap_in) std::swap(Lc.x_re, Lc.x_im);
+            if (a.swap_out) std::swap(Lc.y_re, Lc.y_im);
+            memset(&Lc.a, 0, sizeof Lc.a);
+            Lc.a.m = m;
+            Lc.a.S = gr.S;
+            Lc.a.scale_out = a.swap_out;
+            Lc.a.scale = a.scale;
+            Lc.a.tw = a.tw;
+            Lc.a.tw_cat_top = a.tw_cat_top;
+            Lc.a.tw_top_tab = a.tw_top_tab;
+            Lc.a.coarse = a.coarse;
+            Lc.a.coarse_log = a.coarse_log;
+            Lc.a.fine = a.fine;
+            cudaError_t e = tf(Lc, st);
+            if (e != cudaSuccess) return cuda_fail(e, "TMA pass kernel launch");
+            continue;
+        }
         const int64_t grid = batch * ((n >> gr.L) / TJ);
         cudaError_t e = fn(a, p->algo == SFFT_DIF, first && il, last && il, grid, st);
         if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");

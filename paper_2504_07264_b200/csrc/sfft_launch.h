@@ -9,6 +9,7 @@ namespace sfft {
 struct FusedArgs;
 struct PassArgs;
 struct TmaLaunch;
+struct PassTmaLaunch;
 
 // Launch one fused kernel (N = 2^logn <= 4096) over a.batch rows.
 using FusedLaunchFn = cudaError_t (*)(const FusedArgs &a, bool dif, bool interleaved, cudaStream_t st);
@@ -18,6 +19,9 @@ using PassLaunchFn = cudaError_t (*)(const PassArgs &a, bool dif, bool il_in, bo
 
 // Launch the persistent TMA-fed fused kernel (planar, 16-byte aligned rows).
 using TmaLaunchFn = cudaError_t (*)(const TmaLaunch &L, cudaStream_t st);
+
+// Launch the TMA-pipelined pass kernel (groups with S > 0, planar rows).
+using PassTmaLaunchFn = cudaError_t (*)(const PassTmaLaunch &L, cudaStream_t st);
 
 constexpr int kFusedMaxLog = 12;
 constexpr int kMaxRadixLog = 5;
@@ -40,6 +44,10 @@ TmaLaunchFn tma_launcher_f32(int logn, int lr, bool dif, bool pre);
 TmaLaunchFn tma_launcher_f64(int logn, int lr, bool dif, bool pre);
 int tma_default_lr(int dtype, int logn);   // -1: no TMA config for this size
 void auto_choice(int dtype, int logn, bool *tma, int *lr, bool *pre);  // kernel=auto pick, 0 <= logn <= 12
+
+PassTmaLaunchFn pass_tma_launcher(int dtype, int L, bool dif);
+PassTmaLaunchFn pass_tma_launcher_f32(int L, bool dif);
+PassTmaLaunchFn pass_tma_launcher_f64(int L, bool dif);
 
 void count_launch();
 

@@ -264,3 +264,34 @@ def test_host_pipeline_many_chunks(cuda, monkeypatch, pinned):
         sf.fft_split(re, im, out=(out_r, out_i), inverse=inverse)
         dr, di = sf.fft_split(re.cuda(), im.cuda(), inverse=inverse)
         assert torch.equal(out_r, dr.cpu()) and torch.equal(out_i, di.cpu())
+
+
+@pytest.mark.parametrize("algo", ["dit", "dif"])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("m", [13, 16, 20])
+def test_tma_pass_kernel_opt_in(cuda, m, dtype, algo):
+    # the TMA-pipelined pass kernel (opt-in, SFFT_PASS_TMA=1) in a subprocess
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, torch, sys
+sys.path.insert(0, {repr(__import__('os').path.dirname(__import__('os').path.dirname(__file__)))})
+import paper_2504_07264_b200 as sf
+from oracle import oracle
+rng = np.random.default_rng({m})
+re = rng.standard_normal((3, 1 << {m})).astype(np.{np.dtype(dtype).name})
+im = rng.standard_normal((3, 1 << {m})).astype(np.{np.dtype(dtype).name})
+for inv in (False, True):
+    yr, yi = sf.fft_split(torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda(), algorithm="{algo}", inverse=inv)
+    wr, wi = oracle.fft_split_c(re, im, "{algo}", inv)
+    gr, gi = yr.cpu().numpy().astype(np.float64), yi.cpu().numpy().astype(np.float64)
+    if re.dtype == np.float64:
+        assert np.array_equal(gr.view(np.int64), wr.view(np.int64)) and np.array_equal(gi.view(np.int64), wi.view(np.int64))
+    else:
+        err = np.sqrt(np.sum((gr - wr) ** 2 + (gi - wi) ** 2) / np.sum(wr ** 2 + wi ** 2))
+        assert err <= 1e-5 * {m}, err
+print("ok")
+"""
+    env = dict(__import__('os').environ, SFFT_PASS_TMA="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
