@@ -57,6 +57,9 @@ def parse():
                     help="target CPU time of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"],
+                    help="config 5 on N>1 GPUs: NCCL all-to-all, or phase 0 storing into the peers' "
+                         "symmetric-memory receive buffers (fused exchange)")
     return ap.parse_args()
 
 
@@ -486,11 +489,17 @@ def run_sharded(args):
     sr, si, rr, ri, yr, yi = (torch.empty_like(xr) for _ in range(6))
     ws = torch.empty(plan.workspace_bytes, dtype=torch.uint8, device=device)
 
-    def step():
-        plan.phase(0, xr, xi, sr, si, workspace=ws)
-        dist.all_to_all_single(rr, sr)
-        dist.all_to_all_single(ri, si)
-        plan.phase(1, rr, ri, yr, yi, workspace=ws)
+    if args.transport == "p2p":
+        xch = sdist.P2PExchange(plan)
+
+        def step():
+            xch.run(xr, xi, yr, yi, workspace=ws)
+    else:
+        def step():
+            plan.phase(0, xr, xi, sr, si, workspace=ws)
+            dist.all_to_all_single(rr, sr)
+            dist.all_to_all_single(ri, si)
+            plan.phase(1, rr, ri, yr, yi, workspace=ws)
 
     for _ in range(args.warmup):
         step()
@@ -524,7 +533,9 @@ def run_sharded(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic (seeded per rank)",
             "config": {"workload": cfg.name, "n": cfg.n, "batch": 1,
-                       "parallelism": f"sharded four-step x{world}, NCCL all-to-all of both planes"},
+                       "parallelism": f"sharded four-step x{world}, " + (
+                           "NCCL all-to-all of both planes" if args.transport == "nccl"
+                           else "phase 0 stores into peers' symmetric-memory receive buffers (P2P)")},
             "gbs_algorithmic": 4 * cfg.n * (4 if cfg.dtype == "f32" else 8) / (ms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": moved / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": moved / (ms / 1e3) / 1e9 / peak, "traffic": None,

@@ -144,6 +144,17 @@ int sfft_dist_exec_phase(const sfft_dist_plan *plan, int phase,
                          const void *x_re, const void *x_im, void *y_re,
                          void *y_im, int direction, void *workspace,
                          void *stream);
+/* Phase 0 with the exchange fused into its last launch: instead of writing
+ * the send buffer, the kernel stores each destination segment straight into
+ * that rank's RECEIVE buffer (slot = this rank) through peer pointers
+ * (NVLink/NVSwitch P2P, e.g. torch symmetric memory) -- no separate
+ * all-to-all.  peer_re/peer_im: npeers (= nranks <= 8) device pointers of the
+ * ranks' receive planes.  The caller orders it with a barrier before (peers
+ * done reading) and after (all writes landed) and then runs phase 1. */
+int sfft_dist_exec_phase0_p2p(const sfft_dist_plan *plan, const void *x_re,
+                              const void *x_im, void *const *peer_re,
+                              void *const *peer_im, int npeers, int direction,
+                              void *workspace, void *stream);
 
 /* Host-only helpers (no GPU needed). */
 

@@ -43,6 +43,7 @@ SIGNATURES = {
     "sfft_dist_layout": (_I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I), ctypes.POINTER(_I64)]),
     "sfft_dist_workspace_bytes": (_I, [_P, ctypes.POINTER(ctypes.c_size_t)]),
     "sfft_dist_exec_phase": (_I, [_P, _I, _P, _P, _P, _P, _I, _P, _P]),
+    "sfft_dist_exec_phase0_p2p": (_I, [_P, _P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P), _I, _I, _P, _P]),
 }
 
 

@@ -682,8 +682,32 @@ int sfft_dist_workspace_bytes(const sfft_dist_plan *d, size_t *bytes)
     return SFFT_OK;
 }
 
+static int dist_exec(const sfft_dist_plan *d, int phase, const void *x_re, const void *x_im, void *y_re,
+                     void *y_im, int direction, void *workspace, void *stream, void *const *peer_re,
+                     void *const *peer_im, int npeers);
+
 int sfft_dist_exec_phase(const sfft_dist_plan *d, int phase, const void *x_re, const void *x_im, void *y_re,
                          void *y_im, int direction, void *workspace, void *stream)
+{
+    return dist_exec(d, phase, x_re, x_im, y_re, y_im, direction, workspace, stream, nullptr, nullptr, 0);
+}
+
+int sfft_dist_exec_phase0_p2p(const sfft_dist_plan *d, const void *x_re, const void *x_im, void *const *peer_re,
+                              void *const *peer_im, int npeers, int direction, void *workspace, void *stream)
+{
+    if (!d) return fail(SFFT_EINVAL, "plan is NULL");
+    if (npeers != d->nranks || npeers > 8 || !peer_re || !peer_im)
+        return fail(SFFT_EINVAL, "need one receive buffer per rank (%d, at most 8), got %d", d->nranks, npeers);
+    for (int h = 0; h < npeers; ++h)
+        if (!peer_re[h] || !peer_im[h]) return fail(SFFT_EINVAL, "NULL receive buffer of rank %d", h);
+    // y is unused by the last launch (it stores to the peers); earlier launches use the workspace
+    return dist_exec(d, 0, x_re, x_im, peer_re[0], peer_im[0], direction, workspace, stream, peer_re, peer_im,
+                     npeers);
+}
+
+static int dist_exec(const sfft_dist_plan *d, int phase, const void *x_re, const void *x_im, void *y_re,
+                     void *y_im, int direction, void *workspace, void *stream, void *const *peer_re,
+                     void *const *peer_im, int npeers)
 {
     if (!d) return fail(SFFT_EINVAL, "plan is NULL");
     if (phase != 0 && phase != 1) return fail(SFFT_EINVAL, "phase must be 0 or 1, got %d", phase);
@@ -738,6 +762,14 @@ int sfft_dist_exec_phase(const sfft_dist_plan *d, int phase, const void *x_re, c
             a.in_map = {b, gr.S + (m - L1) - b, -1, m - b};
             if (last) a.out_map = {b, m - b, L1 - b, m - b};   // send layout [dest][n2_local][k1_local]
             else a.out_map = {b, gr.S + gr.L + (m - L1) - b, -1, m - b};
+            if (last && npeers > 0) {   // fused exchange: store into the peers' receive buffers
+                a.npeers = npeers;
+                a.seg_log = m - 2 * b;
+                for (int h = 0; h < npeers; ++h) {
+                    a.peer_re[h] = peer_re[h];
+                    a.peer_im[h] = peer_im[h];
+                }
+            }
         } else {
             // owner field = top b bits of k1 = index mod 2^L1
             a.jpos = L1 - b;

@@ -68,6 +68,12 @@ struct PassArgs {
     // `jrank` in the jb-bit field at bit jpos; addresses go through the maps
     int jb, jpos, jrank;
     AddrMap in_map, out_map;
+    // fused exchange (sfft_dist_exec_phase0_p2p): when npeers > 0 the output
+    // address h*seg + r (send layout) is stored straight into peer h's
+    // receive buffer at slot jrank: peer_{re,im}[h] + jrank*seg + r
+    int npeers;
+    int seg_log;
+    void *peer_re[8], *peer_im[8];
 };
 
 template <typename T, int L, int LR_REQ>
@@ -206,8 +212,21 @@ sfft_pass_kernel(const PassArgs a)
     const T scale = (T)a.scale;
 
     auto put_out = [&](int64_t off, T re, T im) {
-        if (swap_out) dst.store(off, im * scale, re * scale);
-        else dst.store(off, re, im);
+        if (swap_out) {
+            const T t = re;
+            re = im * scale;
+            im = t * scale;
+        }
+        if constexpr (DIST) {
+            if (a.npeers > 0) {   // NVLink/NVSwitch peer store into the receiver's slot
+                const int h = (int)(off >> a.seg_log);
+                const int64_t r = ((int64_t)a.jrank << a.seg_log) + (off & ((int64_t(1) << a.seg_log) - 1));
+                st_stream((T *)a.peer_re[h] + r, re);
+                st_stream((T *)a.peer_im[h] + r, im);
+                return;
+            }
+        }
+        dst.store(off, re, im);
     };
     auto get_in = [&](int64_t off, T &re, T &im) {
         T x, y;

@@ -22,6 +22,13 @@ Two strategies:
    The arithmetic is the reference's radix-2 stages, so an fp64 sharded
    transform is bit-identical to the single-GPU one and to the reference.
 
+   Fused variant (``P2PExchange``): the receive planes live in torch
+   symmetric memory and phase 0's last launch stores each destination
+   segment straight into that rank's receive planes over NVLink/NVSwitch
+   (``DistPlan.phase0_p2p``), so the exchange overlaps the compute tile by
+   tile and the send buffer's HBM round trip disappears; two symmetric-memory
+   barriers order it.
+
 ``fft_dist`` takes an optional ``phase_fn`` so the orchestration (layouts,
 exchange, gather) is testable on CPU with gloo (tests/test_dist_gloo.py).
 """
@@ -101,6 +108,55 @@ class DistPlan:
             _ffi.SFFT_INVERSE if inverse else _ffi.SFFT_FORWARD, workspace.data_ptr(),
             _stream_ptr(self.device)))
         return y_re, y_im
+
+    def phase0_p2p(self, x_re, x_im, recv_re, recv_im, inverse=False, workspace=None):
+        """Phase 0 with the exchange fused in: the last launch stores each
+        destination segment straight into rank h's receive planes
+        (``recv_re[h]``, ``recv_im[h]``: device tensors or raw device
+        pointers of every rank, e.g. symmetric-memory peer buffers)."""
+        if len(recv_re) != self.world or len(recv_im) != self.world:
+            raise ValueError(f"need {self.world} receive buffers per plane")
+        for t in (x_re, x_im):
+            if t.device != self.device or t.dtype != self.dtype or not t.is_contiguous() \
+                    or t.numel() != self.local_elems:
+                raise ValueError("input planes must be contiguous, on the plan's device and dtype, "
+                                 f"with {self.local_elems} elements")
+        ptr = lambda v: v if isinstance(v, int) else v.data_ptr()   # noqa: E731
+        pr = (ctypes.c_void_p * self.world)(*[ptr(v) for v in recv_re])
+        pi = (ctypes.c_void_p * self.world)(*[ptr(v) for v in recv_im])
+        if workspace is None:
+            workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
+        _ffi.check(_ffi.lib.sfft_dist_exec_phase0_p2p(
+            self._handle, x_re.data_ptr(), x_im.data_ptr(), pr, pi, self.world,
+            _ffi.SFFT_INVERSE if inverse else _ffi.SFFT_FORWARD, workspace.data_ptr(),
+            _stream_ptr(self.device)))
+
+
+class P2PExchange:
+    """Receive planes in torch symmetric memory, so phase 0 can store into
+    every peer's buffer directly over NVLink/NVSwitch (the fused exchange).
+    One per (plan, process group); ``run`` = barrier, fused phase 0,
+    barrier, phase 1."""
+
+    def __init__(self, plan: DistPlan, group=None):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        self.plan = plan
+        n = plan.local_elems
+        self.buf = symm_mem.empty(2 * n, dtype=plan.dtype, device=plan.device)
+        grp = group if group is not None else dist.group.WORLD
+        self.handle = symm_mem.rendezvous(self.buf, grp)
+        esz = self.buf.element_size()
+        self.peer_re = [int(p) for p in self.handle.buffer_ptrs]
+        self.peer_im = [int(p) + n * esz for p in self.handle.buffer_ptrs]
+        self.recv_re, self.recv_im = self.buf[:n], self.buf[n:]
+
+    def run(self, x_re, x_im, y_re, y_im, inverse=False, workspace=None):
+        self.handle.barrier(channel=0)          # every rank done reading its receive planes
+        self.plan.phase0_p2p(x_re, x_im, self.peer_re, self.peer_im, inverse=inverse, workspace=workspace)
+        self.handle.barrier(channel=0)          # every store landed
+        return self.plan.phase(1, self.recv_re, self.recv_im, y_re, y_im, inverse=inverse,
+                               workspace=workspace)
 
 
 def scatter_input(x, world, rank, l1):
