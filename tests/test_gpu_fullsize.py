@@ -1,0 +1,169 @@
+"""Parity at the BASELINE.json full sizes (the bench workloads themselves).
+
+At these sizes the oracle cannot transform everything in seconds, so each
+config is checked with (1) the oracle on a seeded sample of rows of the very
+same full-size GPU run (fp64: bitwise), and (2) size-independent properties
+over the whole batch: inverse round trip, Parseval per row, linearity, and
+for config 4 the analytic tone peaks |y[k_j]| ~ N*A_j.  Config 5 (one
+2^28-point transform) checks round trip, Parseval and a few bins against a
+direct fp64 DFT sum, single-GPU and sharded (8 emulated ranks).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2504_07264_b200 as sf
+import workloads
+from oracle import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_l2(a_re, a_im, b_re, b_im):
+    num = np.sqrt(np.sum((a_re - b_re) ** 2 + (a_im - b_im) ** 2))
+    return num / np.sqrt(np.sum(b_re ** 2 + b_im ** 2))
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.int64)
+
+
+def full_run(name):
+    cfg = workloads.CONFIGS[name]
+    re, im = workloads.generate(cfg)
+    tdt = torch.float32 if cfg.dtype == "f32" else torch.float64
+    xr = torch.from_numpy(re).cuda()
+    xi = torch.from_numpy(im).cuda()
+    plan = sf.make_plan(cfg.log2n, dtype=tdt, device="cuda:0")
+    yr, yi = sf.fft_split(xr, xi, plan=plan)
+    return cfg, re, im, xr, xi, yr, yi, plan
+
+
+def check_sample_rows(cfg, re, im, yr, yi, rows):
+    gr = yr[rows].cpu().numpy().astype(np.float64)
+    gi = yi[rows].cpu().numpy().astype(np.float64)
+    wr, wi = oracle.fft_split_c(re[rows], im[rows])
+    if cfg.dtype == "f64":
+        assert np.array_equal(bits(gr), bits(wr)) and np.array_equal(bits(gi), bits(wi))
+    else:
+        assert rel_l2(gr, gi, wr, wi) <= 1e-5 * cfg.log2n
+
+
+def check_properties(cfg, xr, xi, yr, yi, plan):
+    tol = 1e-5 * cfg.log2n if cfg.dtype == "f32" else 1e-12
+    # inverse round trip over the whole batch
+    zr, zi = sf.ifft_split(yr, yi, plan=plan)
+    num = torch.sqrt(torch.sum((zr - xr).double() ** 2 + (zi - xi).double() ** 2))
+    den = torch.sqrt(torch.sum(xr.double() ** 2 + xi.double() ** 2))
+    assert (num / den).item() <= tol
+    # Parseval, every row
+    ex = (xr.double() ** 2 + xi.double() ** 2).sum(dim=1)
+    ey = (yr.double() ** 2 + yi.double() ** 2).sum(dim=1) / cfg.n
+    assert torch.max(torch.abs(ex - ey) / ex).item() <= tol
+    # linearity on a block of rows: F(a x + b y) = a F(x) + b F(y)
+    k = min(4096, xr.shape[0] // 2)
+    a, b = 0.75, -1.5
+    cr = a * xr[:k] + b * xr[k:2 * k]
+    ci = a * xi[:k] + b * xi[k:2 * k]
+    fr, fi = sf.fft_split(cr, ci, plan=plan)
+    lr_ = a * yr[:k] + b * yr[k:2 * k]
+    li_ = a * yi[:k] + b * yi[k:2 * k]
+    num = torch.sqrt(torch.sum((fr - lr_).double() ** 2 + (fi - li_).double() ** 2))
+    den = torch.sqrt(torch.sum(lr_.double() ** 2 + li_.double() ** 2))
+    assert (num / den).item() <= 4 * tol
+
+
+@pytest.mark.parametrize("name", ["cfg2_n64_f32", "cfg3_n1024_f32", "cfg3_n1024_f64"])
+def test_full_batch_config(cuda, name):
+    cfg, re, im, xr, xi, yr, yi, plan = full_run(name)
+    rng = np.random.default_rng(99)
+    rows = np.unique(np.concatenate([np.arange(64), rng.integers(0, cfg.batch, 448),
+                                     np.arange(cfg.batch - 64, cfg.batch)]))
+    check_sample_rows(cfg, re, im, yr, yi, rows)
+    check_properties(cfg, xr, xi, yr, yi, plan)
+
+
+def test_full_batch_config1(cuda):
+    # BASELINE configs[0] (the reference's own CPU case) in full, bitwise vs golden
+    import os
+    gold = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_vectors.npz"))
+    cfg, re, im, xr, xi, yr, yi, plan = full_run("cfg1_n8_f64")
+    assert np.array_equal(bits(yr.cpu().numpy()), bits(gold["cfg1_dit_re"]))
+    assert np.array_equal(bits(yi.cpu().numpy()), bits(gold["cfg1_dit_im"]))
+
+
+def test_full_batch_config4_tones(cuda):
+    cfg, re, im, xr, xi, yr, yi, plan = full_run("cfg4_n4096_f32")
+    rng = np.random.default_rng(cfg.seed)
+    k, amp, phi = workloads.tone_params(cfg, rng)
+    mag = torch.sqrt(yr.double() ** 2 + yi.double() ** 2)
+    peaks = torch.gather(mag, 1, torch.from_numpy(k).cuda()).cpu().numpy()
+    # expected: the coherent sum of the tones that share a bin, plus noise
+    # (sigma 0.01 per sample -> ~0.01*sqrt(2N) ~ 0.9 in a bin)
+    coef = amp * np.exp(1j * phi)
+    want = np.empty_like(peaks)
+    for t in range(8):
+        want[:, t] = np.abs(np.sum(np.where(k == k[:, t:t + 1], coef, 0), axis=1)) * cfg.n
+    assert np.max(np.abs(peaks - want)) <= 8.0
+    # every other bin holds only noise
+    mag[torch.arange(cfg.batch, device="cuda")[:, None], torch.from_numpy(k).cuda()] = 0
+    assert mag.max().item() <= 8.0
+    check_sample_rows(cfg, re, im, yr, yi, np.arange(0, cfg.batch, 4096))
+    check_properties(cfg, xr, xi, yr, yi, plan)
+
+
+def test_config5_single_transform(cuda):
+    cfg, re, im, xr, xi, yr, yi, plan = full_run("cfg5_n2p28_f32")
+    check_properties_1d(cfg, xr, xi, yr, yi, plan)
+    # a few bins against a direct fp64 DFT sum of the same fp32 input
+    x = re[0].astype(np.float64) + 1j * im[0].astype(np.float64)
+    n = cfg.n
+    idx = np.arange(n, dtype=np.int64)
+    for kb in (0, 1, 12345, n // 2 + 7):
+        w = np.exp(-2j * np.pi * ((kb * idx) % n) / n)
+        want = np.sum(x * w)
+        got = complex(yr[0, kb].item(), yi[0, kb].item())
+        assert abs(got - want) <= 1e-5 * cfg.log2n * np.sqrt(np.sum(np.abs(x) ** 2))
+
+
+def check_properties_1d(cfg, xr, xi, yr, yi, plan):
+    tol = 1e-5 * cfg.log2n
+    zr, zi = sf.ifft_split(yr, yi, plan=plan)
+    num = torch.sqrt(torch.sum((zr - xr).double() ** 2 + (zi - xi).double() ** 2))
+    den = torch.sqrt(torch.sum(xr.double() ** 2 + xi.double() ** 2))
+    assert (num / den).item() <= tol
+    ex = (xr.double() ** 2 + xi.double() ** 2).sum()
+    ey = (yr.double() ** 2 + yi.double() ** 2).sum() / cfg.n
+    assert abs((ex - ey) / ex).item() <= tol
+
+
+def test_config5_sharded_eight_ranks_matches_single_gpu(cuda):
+    from paper_2504_07264_b200 import dist
+    cfg = workloads.CONFIGS["cfg5_n2p28_f32"]
+    m, world = cfg.log2n, 8
+    re, im = workloads.generate(cfg)
+    x_re, x_im = re[0], im[0]
+    plans = [dist.DistPlan(m, world, r, dtype=torch.float32, device="cuda:0") for r in range(world)]
+    l1, nl = plans[0].l1, plans[0].local_elems
+    recv_re = [torch.empty(nl, device="cuda:0") for _ in range(world)]
+    recv_im = [torch.empty(nl, device="cuda:0") for _ in range(world)]
+    for r, p in enumerate(plans):
+        lr = torch.as_tensor(np.ascontiguousarray(dist.scatter_input(x_re, world, r, l1))).cuda().reshape(-1)
+        li = torch.as_tensor(np.ascontiguousarray(dist.scatter_input(x_im, world, r, l1))).cuda().reshape(-1)
+        p.phase0_p2p(lr, li, recv_re, recv_im)
+        del lr, li
+    outs_r, outs_i = [], []
+    shape = (1 << (m - l1), (1 << l1) // world)
+    for h, p in enumerate(plans):
+        yr, yi = torch.empty_like(recv_re[h]), torch.empty_like(recv_im[h])
+        p.phase(1, recv_re[h], recv_im[h], yr, yi)
+        outs_r.append(yr.reshape(shape))
+        outs_i.append(yi.reshape(shape))
+    del recv_re, recv_im
+    gr = dist.gather_output(outs_r, l1)
+    gi = dist.gather_output(outs_i, l1)
+    sr, si = sf.fft_split(torch.from_numpy(x_re).cuda(), torch.from_numpy(x_im).cuda())
+    num = torch.sqrt(torch.sum((gr - sr).double() ** 2 + (gi - si).double() ** 2))
+    den = torch.sqrt(torch.sum(sr.double() ** 2 + si.double() ** 2))
+    assert (num / den).item() <= 1e-6
