@@ -178,21 +178,117 @@ __device__ __forceinline__ void load_bases(vec2_t<T> *pre, int gs, typename TW::
     for (int t = 1; t <= K; ++t) pre[t - 1] = tw.get(gs + t, cbase);
 }
 
-// K consecutive DIT stages (global stages gs+1 .. gs+K) on the 2^K values
-// v[0..2^K) of one virtual thread.  Register position p holds, before stage
-// t, the (size 2^(gs+t-1)) partial transform of sub-sequence (p mod
-// 2^K/2^(t-1)) at frequency index rev_{t-1}(p / (2^K/2^(t-1))); the
-// stage-(gs+t) factor index is q = cbase + (f << gs).  After the K stages
-// register rev_K(f) holds output frequency f.  Validated bitwise against the
-// reference by tests/test_schedule_model.py (a numpy restatement of exactly
-// this index map).
-// TRIV = false promises gs >= 1 and no trivial factors to skip (every pass
-// group after the first), which removes the per-stage kind tests.
-template <typename T, int K, bool TRIV = true, typename TW>
-__device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw,
-                                           const vec2_t<T> *pre = nullptr)
+// Packed fp32 pair arithmetic (sm_100a FADD2/FMUL2/FFMA2): each lane is
+// rounded exactly like the scalar instruction, so the packed path is
+// bit-identical to the scalar one -- it only halves the instruction count.
+__device__ __forceinline__ unsigned long long f2u(float2 a) { return *reinterpret_cast<unsigned long long *>(&a); }
+__device__ __forceinline__ float2 u2f(unsigned long long a) { return *reinterpret_cast<float2 *>(&a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b)
+{
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 sub2(float2 a, float2 b)
+{
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b)
+{
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c)
+{
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(d);
+}
+
+// c = b * w for a complex value held as (re, im), numpy's rounding:
+// (fma(br, wr, -(bi*wi)), fma(br, wi, bi*wr)).  `wq` = (-wi, wr) precomputed.
+__device__ __forceinline__ float2 cmulv(float2 b, float2 w, float2 wq)
+{
+    const float2 q = mul2(make_float2(b.y, b.y), wq);          // (-(bi*wi), bi*wr), exact negation
+    return fma2(make_float2(b.x, b.x), w, q);
+}
+__device__ __forceinline__ double2 cmulv(double2 b, double2 w, double2)
+{
+    double2 c;
+    cmul(b.x, b.y, w.x, w.y, c.x, c.y);
+    return c;
+}
+__device__ __forceinline__ float2 addv(float2 a, float2 b) { return add2(a, b); }
+__device__ __forceinline__ float2 subv(float2 a, float2 b) { return sub2(a, b); }
+__device__ __forceinline__ double2 addv(double2 a, double2 b) { return make_double2(add_rn(a.x, b.x), add_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 subv(double2 a, double2 b) { return make_double2(sub_rn(a.x, b.x), sub_rn(a.y, b.y)); }
+
+// Scalar fp32 forms (same rounding), for kernels where the packed
+// instructions' longer dependency chains cost more than the issue slots they
+// save (latency-bound shapes; chosen per kernel).
+__device__ __forceinline__ float2 cmuls(float2 b, float2 w)
+{
+    float2 c;
+    cmul(b.x, b.y, w.x, w.y, c.x, c.y);
+    return c;
+}
+__device__ __forceinline__ double2 cmuls(double2 b, double2 w) { return cmulv(b, w, w); }
+__device__ __forceinline__ float2 adds(float2 a, float2 b) { return make_float2(add_rn(a.x, b.x), add_rn(a.y, b.y)); }
+__device__ __forceinline__ float2 subs(float2 a, float2 b) { return make_float2(sub_rn(a.x, b.x), sub_rn(a.y, b.y)); }
+__device__ __forceinline__ double2 adds(double2 a, double2 b) { return addv(a, b); }
+__device__ __forceinline__ double2 subs(double2 a, double2 b) { return subv(a, b); }
+
+template <bool PACK, typename V>
+__device__ __forceinline__ V vadd(V a, V b) { if constexpr (PACK) return addv(a, b); else return adds(a, b); }
+template <bool PACK, typename V>
+__device__ __forceinline__ V vsub(V a, V b) { if constexpr (PACK) return subv(a, b); else return subs(a, b); }
+template <bool PACK, typename V>
+__device__ __forceinline__ V vmul(V b, V w, V wq) { if constexpr (PACK) return cmulv(b, w, wq); else return cmuls(b, w); }
+
+template <typename T>
+__device__ __forceinline__ vec2_t<T> wquad(vec2_t<T> w)
+{
+    vec2_t<T> q;
+    q.x = -w.y;
+    q.y = w.x;
+    return q;
+}
+
+// Factor of stage t (= i - gs), index f, of a virtual thread with base
+// factor `base` = w_i(cbase) (see dit_stages).
+template <typename T, typename TW>
+__device__ __forceinline__ vec2_t<T> stage_factor(int t, int f, int i, bool first, typename TW::index_t cbase,
+                                                  int gs, const TW &tw, vec2_t<T> base)
 {
     using I = typename TW::index_t;
+    if (first) return SmallTw<T>::get((1 << (t - 1)) - 1 + f);
+    if (FactorTw<T>::value) {
+        if (f == 0) return base;
+        const vec2_t<T> s = SmallTw<T>::get((1 << (t - 1)) - 1 + f);
+        vec2_t<T> w;
+        cmul(base.x, base.y, s.x, s.y, w.x, w.y);
+        return w;
+    }
+    return tw.get(i, cbase + ((I)f << gs));
+}
+
+// K consecutive DIT stages (global stages gs+1 .. gs+K) on the 2^K complex
+// values v[0..2^K) (re, im) of one virtual thread.  Register position p
+// holds, before stage t, the (size 2^(gs+t-1)) partial transform of
+// sub-sequence (p mod 2^K/2^(t-1)) at frequency index
+// rev_{t-1}(p / (2^K/2^(t-1))); the stage-(gs+t) factor index is
+// q = cbase + (f << gs).  After the K stages register rev_K(f) holds output
+// frequency f.  Validated bitwise against the reference by
+// tests/test_schedule_model.py (a numpy restatement of this index map).
+// TRIV = false promises gs >= 1 and no trivial factors to skip (every pass
+// group after the first), which removes the per-stage kind tests.
+template <typename T, int K, bool TRIV = true, bool PACK = true, typename TW>
+__device__ __forceinline__ void dit_stages(vec2_t<T> *v, int gs, typename TW::index_t cbase, const TW &tw,
+                                           const vec2_t<T> *pre = nullptr)
+{
     const bool first = TRIV && gs == 0;   // first pass: every factor is a compile-time constant
 #pragma unroll
     for (int t = 1; t <= K; ++t) {
@@ -208,38 +304,25 @@ __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::in
                            : i == 1 ? 0
                            : (SkipTrivial<T>::value && first && f == 0) ? 1
                            : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
-            vec2_t<T> w;
+            vec2_t<T> w, wq;
             if (kind == 3) {
-                if (first) {
-                    w = SmallTw<T>::get((1 << (t - 1)) - 1 + f);
-                } else if (FactorTw<T>::value) {
-                    if (f == 0) {
-                        w = base;
-                    } else {
-                        const vec2_t<T> s = SmallTw<T>::get((1 << (t - 1)) - 1 + f);
-                        cmul(base.x, base.y, s.x, s.y, w.x, w.y);
-                    }
-                } else {
-                    w = tw.get(i, cbase + ((I)f << gs));
-                }
+                w = stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                wq = wquad<T>(w);
             }
 #pragma unroll
             for (int r = 0; r < half; ++r) {
                 const int p1 = r + rf, p2 = p1 + half;
-                T tr, ti;
+                vec2_t<T> tt;
                 if (kind == 3) {
-                    cmul(vr[p2], vi[p2], w.x, w.y, tr, ti);
+                    tt = vmul<PACK>(v[p2], w, wq);
                 } else if (kind == 2) {
-                    tr = vi[p2];
-                    ti = -vr[p2];
+                    tt.x = v[p2].y;
+                    tt.y = -v[p2].x;
                 } else {
-                    tr = vr[p2];
-                    ti = vi[p2];
+                    tt = v[p2];
                 }
-                vr[p2] = sub_rn(vr[p1], tr);
-                vi[p2] = sub_rn(vi[p1], ti);
-                vr[p1] = add_rn(vr[p1], tr);
-                vi[p1] = add_rn(vi[p1], ti);
+                v[p2] = vsub<PACK>(v[p1], tt);
+                v[p1] = vadd<PACK>(v[p1], tt);
             }
         }
     }
@@ -247,11 +330,10 @@ __device__ __forceinline__ void dit_stages(T *vr, T *vi, int gs, typename TW::in
 
 // Transpose of dit_stages: DIF stages gs+K .. gs+1 (descending), same
 // register map run backwards.
-template <typename T, int K, bool TRIV = true, typename TW>
-__device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, typename TW::index_t cbase, const TW &tw,
+template <typename T, int K, bool TRIV = true, bool PACK = true, typename TW>
+__device__ __forceinline__ void dif_stages(vec2_t<T> *v, int gs, typename TW::index_t cbase, const TW &tw,
                                            const vec2_t<T> *pre = nullptr)
 {
-    using I = typename TW::index_t;
     const bool first = TRIV && gs == 0;
 #pragma unroll
     for (int t = K; t >= 1; --t) {
@@ -266,36 +348,23 @@ __device__ __forceinline__ void dif_stages(T *vr, T *vi, int gs, typename TW::in
                            : i == 1 ? 0
                            : (SkipTrivial<T>::value && first && f == 0) ? 1
                            : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
-            vec2_t<T> w;
+            vec2_t<T> w, wq;
             if (kind == 3) {
-                if (first) {
-                    w = SmallTw<T>::get((1 << (t - 1)) - 1 + f);
-                } else if (FactorTw<T>::value) {
-                    if (f == 0) {
-                        w = base;
-                    } else {
-                        const vec2_t<T> s = SmallTw<T>::get((1 << (t - 1)) - 1 + f);
-                        cmul(base.x, base.y, s.x, s.y, w.x, w.y);
-                    }
-                } else {
-                    w = tw.get(i, cbase + ((I)f << gs));
-                }
+                w = stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                wq = wquad<T>(w);
             }
 #pragma unroll
             for (int r = 0; r < half; ++r) {
                 const int p1 = r + rf, p2 = p1 + half;
-                const T tr = sub_rn(vr[p1], vr[p2]);
-                const T ti = sub_rn(vi[p1], vi[p2]);
-                vr[p1] = add_rn(vr[p1], vr[p2]);
-                vi[p1] = add_rn(vi[p1], vi[p2]);
+                const vec2_t<T> d = vsub<PACK>(v[p1], v[p2]);
+                v[p1] = vadd<PACK>(v[p1], v[p2]);
                 if (kind == 3) {
-                    cmul(tr, ti, w.x, w.y, vr[p2], vi[p2]);
+                    v[p2] = vmul<PACK>(d, w, wq);
                 } else if (kind == 2) {
-                    vr[p2] = ti;
-                    vi[p2] = -tr;
+                    v[p2].x = d.y;
+                    v[p2].y = -d.x;
                 } else {
-                    vr[p2] = tr;
-                    vi[p2] = ti;
+                    v[p2] = d;
                 }
             }
         }

@@ -119,7 +119,7 @@ __device__ __forceinline__ void sig_sync()
 
 // ---- DIT pass p -----------------------------------------------------------
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
-__device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool valid,
+__device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool valid,
                                          T *sr, T *si, const GIO<T, IL> &io,
                                          const TwCat<T> &tw, const vec2_t<T> *pre)
 {
@@ -138,11 +138,11 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
         for (int r = 0; r < RP; ++r) {
             const int e = j + r * (N / RP);
             if constexpr (FIRST) {
-                if (valid) io.load(row, e, vr[u * RP + r], vi[u * RP + r]);
-                else { vr[u * RP + r] = T(0); vi[u * RP + r] = T(0); }
+                if (valid) io.load(row, e, v[u * RP + r].x, v[u * RP + r].y);
+                else { v[u * RP + r].x = T(0); v[u * RP + r].y = T(0); }
             } else {
-                vr[u * RP + r] = sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
-                vi[u * RP + r] = si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
+                v[u * RP + r].x = sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
+                v[u * RP + r].y = si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
             }
         }
     }
@@ -150,7 +150,7 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = t + P * u;
-        dit_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (j & (NS - 1)), tw,
+        dit_stages<T, KP>(v + u * RP, SP, (j & (NS - 1)), tw,
                           (pre && p > 0) ? pre + p * R + u * KP : nullptr);
     }
     // scatter in Stockham order
@@ -163,8 +163,8 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
 #pragma unroll
             for (int f = 0; f < RP; ++f) {
                 const int e = base + NS * f;
-                sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = vr[u * RP + brev(f, KP)];
-                si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = vi[u * RP + brev(f, KP)];
+                sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].x;
+                si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].y;
             }
         }
         sig_sync<P>();
@@ -175,26 +175,26 @@ __device__ __forceinline__ void dit_pass(T *vr, T *vi, int t, int64_t row, bool 
                 const int j = t + P * u;     // NS*RP == N here, so (j >> SP) == 0
 #pragma unroll
                 for (int f = 0; f < RP; ++f)
-                    io.store(row, j + NS * f, vr[u * RP + brev(f, KP)], vi[u * RP + brev(f, KP)]);
+                    io.store(row, j + NS * f, v[u * RP + brev(f, KP)].x, v[u * RP + brev(f, KP)].y);
             }
         }
     }
 }
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
-__device__ __forceinline__ void dit_from(T *vr, T *vi, int t, int64_t row, bool valid,
+__device__ __forceinline__ void dit_from(vec2_t<T> *v, int t, int64_t row, bool valid,
                                          T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw,
                                          const vec2_t<T> *pre)
 {
     if constexpr (p < FusedShape<LOGN, LR_REQ>::NPASS) {
-        dit_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw, pre);
-        dit_from<T, LOGN, LR_REQ, IL, p + 1>(vr, vi, t, row, valid, sr, si, io, tw, pre);
+        dit_pass<T, LOGN, LR_REQ, IL, p>(v, t, row, valid, sr, si, io, tw, pre);
+        dit_from<T, LOGN, LR_REQ, IL, p + 1>(v, t, row, valid, sr, si, io, tw, pre);
     }
 }
 
 // ---- DIF pass p (executed for p = NPASS-1 .. 0) --------------------------
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
-__device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool valid,
+__device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool valid,
                                          T *sr, T *si, const GIO<T, IL> &io,
                                          const TwCat<T> &tw, const vec2_t<T> *pre)
 {
@@ -214,18 +214,18 @@ __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool 
             const int e = base + NS * f;
             const int d = u * RP + brev(f, KP);
             if constexpr (FIRST) {
-                if (valid) io.load(row, e, vr[d], vi[d]);
-                else { vr[d] = T(0); vi[d] = T(0); }
+                if (valid) io.load(row, e, v[d].x, v[d].y);
+                else { v[d].x = T(0); v[d].y = T(0); }
             } else {
-                vr[d] = sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
-                vi[d] = si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
+                v[d].x = sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
+                v[d].y = si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
             }
         }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = t + P * u;
-        dif_stages<T, KP>(vr + u * RP, vi + u * RP, SP, (j & (NS - 1)), tw,
+        dif_stages<T, KP>(v + u * RP, SP, (j & (NS - 1)), tw,
                           (pre && p > 0) ? pre + p * R + u * KP : nullptr);
     }
     if constexpr (!LAST) {
@@ -236,8 +236,8 @@ __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool 
 #pragma unroll
             for (int r = 0; r < RP; ++r) {
                 const int e = j + r * (N / RP);
-                sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = vr[u * RP + r];
-                si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = vi[u * RP + r];
+                sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].x;
+                si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].y;
             }
         }
         sig_sync<P>();
@@ -248,20 +248,20 @@ __device__ __forceinline__ void dif_pass(T *vr, T *vi, int t, int64_t row, bool 
                 const int j = t + P * u;
 #pragma unroll
                 for (int r = 0; r < RP; ++r)
-                    io.store(row, j + r * (N / RP), vr[u * RP + r], vi[u * RP + r]);
+                    io.store(row, j + r * (N / RP), v[u * RP + r].x, v[u * RP + r].y);
             }
         }
     }
 }
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
-__device__ __forceinline__ void dif_from(T *vr, T *vi, int t, int64_t row, bool valid,
+__device__ __forceinline__ void dif_from(vec2_t<T> *v, int t, int64_t row, bool valid,
                                          T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw,
                                          const vec2_t<T> *pre)
 {
     if constexpr (p >= 0) {
-        dif_pass<T, LOGN, LR_REQ, IL, p>(vr, vi, t, row, valid, sr, si, io, tw, pre);
-        dif_from<T, LOGN, LR_REQ, IL, p - 1>(vr, vi, t, row, valid, sr, si, io, tw, pre);
+        dif_pass<T, LOGN, LR_REQ, IL, p>(v, t, row, valid, sr, si, io, tw, pre);
+        dif_from<T, LOGN, LR_REQ, IL, p - 1>(v, t, row, valid, sr, si, io, tw, pre);
     }
 }
 
@@ -291,7 +291,7 @@ sfft_fused_kernel(const FusedArgs a)
             io.store(row, 0, re, im);
         }
     } else {
-        T vr[R], vi[R];
+        vec2_t<T> v[R];
         T *sr = sbase + sl * SSTR;
         T *si = sbase + S * SSTR + sl * SSTR;
         // fp32: the base factors of passes >= 1, fetched before any data
@@ -311,10 +311,10 @@ sfft_fused_kernel(const FusedArgs a)
             }
         }
         if constexpr (DIF)
-            dif_from<T, LOGN, LR_REQ, IL, Sh::NPASS - 1>(vr, vi, t, row, valid, sr, si, io, tw,
+            dif_from<T, LOGN, LR_REQ, IL, Sh::NPASS - 1>(v, t, row, valid, sr, si, io, tw,
                                                          (PRE && FactorTw<T>::value) ? pre : nullptr);
         else
-            dit_from<T, LOGN, LR_REQ, IL, 0>(vr, vi, t, row, valid, sr, si, io, tw,
+            dit_from<T, LOGN, LR_REQ, IL, 0>(v, t, row, valid, sr, si, io, tw,
                                              (PRE && FactorTw<T>::value) ? pre : nullptr);
     }
 }

@@ -235,7 +235,7 @@ sfft_pass_kernel(const PassArgs a)
         im = swap_in ? x : y;
     };
 
-    T vr[R], vi[R];
+    vec2_t<T> v[R];
 
     // fp32 groups after the first: every base factor of every internal pass,
     // fetched up front (independent of the data) -- pre[pass][u*K + t-1]
@@ -279,17 +279,17 @@ sfft_pass_kernel(const PassArgs a)
             _Pragma("unroll") for (int r = 0; r < RP; ++r)                                      \
             {                                                                                   \
                 const int e = jp + r * (SUB / RP);                                              \
-                if (pp == 0) get_in(iaddr(j + (uint32_t)e * NJ), vr[u * RP + r], vi[u * RP + r]); \
+                if (pp == 0) get_in(iaddr(j + (uint32_t)e * NJ), v[u * RP + r].x, v[u * RP + r].y); \
                 else {                                                                          \
-                    vr[u * RP + r] = sr[e * RS + jl];                                           \
-                    vi[u * RP + r] = si[e * RS + jl];                                           \
+                    v[u * RP + r].x = sr[e * RS + jl];                                           \
+                    v[u * RP + r].y = si[e * RS + jl];                                           \
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                           \
         {                                                                                       \
             const int jp = t + P * u;                                                           \
-            dit_stages<T, KP, S0>(vr + u * RP, vi + u * RP, S + sp,                             \
+            dit_stages<T, KP, S0>(v + u * RP, S + sp,                             \
                                   (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw,               \
                                   PRE ? &pre[pp][u * KP] : nullptr);                            \
         }                                                                                       \
@@ -303,8 +303,8 @@ sfft_pass_kernel(const PassArgs a)
                 _Pragma("unroll") for (int f = 0; f < RP; ++f)                                  \
                 {                                                                               \
                     const int e = base + nsp * f;                                               \
-                    sr[e * RS + jl] = vr[u * RP + brev(f, KP)];                                 \
-                    si[e * RS + jl] = vi[u * RP + brev(f, KP)];                                 \
+                    sr[e * RS + jl] = v[u * RP + brev(f, KP)].x;                                 \
+                    si[e * RS + jl] = v[u * RP + brev(f, KP)].y;                                 \
                 }                                                                               \
             }                                                                                   \
             __syncthreads();                                                                    \
@@ -315,8 +315,8 @@ sfft_pass_kernel(const PassArgs a)
                 _Pragma("unroll") for (int f = 0; f < RP; ++f)                                  \
                 {                                                                               \
                     const uint32_t o = jp + nsp * f;                                            \
-                    put_out(oaddr(gbase + ns * o), vr[u * RP + brev(f, KP)],                    \
-                            vi[u * RP + brev(f, KP)]);                                          \
+                    put_out(oaddr(gbase + ns * o), v[u * RP + brev(f, KP)].x,                    \
+                            v[u * RP + brev(f, KP)].y);                                          \
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \
@@ -368,17 +368,17 @@ sfft_pass_kernel(const PassArgs a)
             {                                                                                   \
                 const int e = base + nsp * f;                                                   \
                 const int d = u * RP + brev(f, KP);                                             \
-                if (first && !S0) get_in(iaddr(gbase + ns * (uint32_t)e), vr[d], vi[d]);        \
+                if (first && !S0) get_in(iaddr(gbase + ns * (uint32_t)e), v[d].x, v[d].y);        \
                 else {                                                                          \
-                    vr[d] = sr[e * RS + jl];                                                    \
-                    vi[d] = si[e * RS + jl];                                                    \
+                    v[d].x = sr[e * RS + jl];                                                    \
+                    v[d].y = si[e * RS + jl];                                                    \
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                           \
         {                                                                                       \
             const int jp = t + P * u;                                                           \
-            dif_stages<T, KP, S0>(vr + u * RP, vi + u * RP, S + sp,                             \
+            dif_stages<T, KP, S0>(v + u * RP, S + sp,                             \
                                   (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw,               \
                                   PRE ? &pre[pp][u * KP] : nullptr);                            \
         }                                                                                       \
@@ -390,8 +390,8 @@ sfft_pass_kernel(const PassArgs a)
                 _Pragma("unroll") for (int r = 0; r < RP; ++r)                                  \
                 {                                                                               \
                     const int e = jp + r * (SUB / RP);                                          \
-                    sr[e * RS + jl] = vr[u * RP + r];                                           \
-                    si[e * RS + jl] = vi[u * RP + r];                                           \
+                    sr[e * RS + jl] = v[u * RP + r].x;                                           \
+                    si[e * RS + jl] = v[u * RP + r].y;                                           \
                 }                                                                               \
             }                                                                                   \
             __syncthreads();                                                                    \
@@ -402,7 +402,7 @@ sfft_pass_kernel(const PassArgs a)
                 _Pragma("unroll") for (int r = 0; r < RP; ++r)                                  \
                 {                                                                               \
                     const int e = jp + r * (SUB / RP);                                          \
-                    put_out(oaddr(j + (uint32_t)e * NJ), vr[u * RP + r], vi[u * RP + r]);       \
+                    put_out(oaddr(j + (uint32_t)e * NJ), v[u * RP + r].x, v[u * RP + r].y);       \
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \

@@ -91,7 +91,7 @@ sfft_pass_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_con
     constexpr int SUB = Sh::SUB, LR = Sh::LR, R = Sh::R, P = Sh::P, TJ = Sh::TJ, NPI = Sh::NPI,
                   PLANE = Sh::PLANE, BUF = Sh::BUF;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + Sh::BAR_OFF);
 
     const int tid = threadIdx.x;
@@ -151,7 +151,7 @@ sfft_pass_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_con
         for (int s = 0; s < STAGES - 1 && s < nk; ++s) load_tile(s, blockIdx.x + (int64_t)s * gridDim.x);
     }
 
-    T vr[R], vi[R];
+    vec2_t<T> v[R];
     for (int64_t k = 0; k < nk; ++k) {
         const int st = (int)(k % STAGES);
         const int64_t tile = blockIdx.x + k * gridDim.x;
@@ -179,14 +179,14 @@ sfft_pass_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_con
             _Pragma("unroll") for (int r = 0; r < RP; ++r)                                      \
             {                                                                                   \
                 const int e = jp + r * (SUB / RP);                                              \
-                vr[u * RP + r] = lds_at<T>(br, swz_row<T>(e, jl));                              \
-                vi[u * RP + r] = lds_at<T>(bi, swz_row<T>(e, jl));                              \
+                v[u * RP + r].x = lds_at<T>(br, swz_row<T>(e, jl));                              \
+                v[u * RP + r].y = lds_at<T>(bi, swz_row<T>(e, jl));                              \
             }                                                                                   \
         }                                                                                       \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                           \
         {                                                                                       \
             const int jp = t + P * u;                                                           \
-            dit_stages<T, KP, false>(vr + u * RP, vi + u * RP, S + sp,                          \
+            dit_stages<T, KP, false>(v + u * RP, S + sp,                          \
                                      (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw);           \
         }                                                                                       \
         __syncthreads();                                                                        \
@@ -198,7 +198,7 @@ sfft_pass_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_con
             _Pragma("unroll") for (int f = 0; f < RP; ++f)                                      \
             {                                                                                   \
                 const int e = base + nsp * f;                                                   \
-                T re = vr[u * RP + brev(f, KP)], im = vi[u * RP + brev(f, KP)];                 \
+                T re = v[u * RP + brev(f, KP)].x, im = v[u * RP + brev(f, KP)].y;                 \
                 if (last && do_scale) { re *= scale; im *= scale; }                             \
                 sts_at<T>(br, swz_row<T>(e, jl), re);                                           \
                 sts_at<T>(bi, swz_row<T>(e, jl), im);                                           \
@@ -230,14 +230,14 @@ sfft_pass_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_con
             {                                                                                   \
                 const int e = base + nsp * f;                                                   \
                 const int d = u * RP + brev(f, KP);                                             \
-                vr[d] = lds_at<T>(br, swz_row<T>(e, jl));                                       \
-                vi[d] = lds_at<T>(bi, swz_row<T>(e, jl));                                       \
+                v[d].x = lds_at<T>(br, swz_row<T>(e, jl));                                       \
+                v[d].y = lds_at<T>(bi, swz_row<T>(e, jl));                                       \
             }                                                                                   \
         }                                                                                       \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                           \
         {                                                                                       \
             const int jp = t + P * u;                                                           \
-            dif_stages<T, KP, false>(vr + u * RP, vi + u * RP, S + sp,                          \
+            dif_stages<T, KP, false>(v + u * RP, S + sp,                          \
                                      (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw);           \
         }                                                                                       \
         __syncthreads();                                                                        \
@@ -248,7 +248,7 @@ sfft_pass_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_con
             _Pragma("unroll") for (int r = 0; r < RP; ++r)                                      \
             {                                                                                   \
                 const int e = jp + r * (SUB / RP);                                              \
-                T re = vr[u * RP + r], im = vi[u * RP + r];                                     \
+                T re = v[u * RP + r].x, im = v[u * RP + r].y;                                     \
                 if (last && do_scale) { re *= scale; im *= scale; }                             \
                 sts_at<T>(br, swz_row<T>(e, jl), re);                                           \
                 sts_at<T>(bi, swz_row<T>(e, jl), im);                                           \

@@ -22,6 +22,17 @@
 
 namespace sfft {
 
+// Measured back to back on cfg2 (tools/ab_launch2.sh): this kernel runs
+// 172 us per 1 GiB step with scalar fp32 math and generic-pointer shared
+// accesses, 190 us with packed FFMA2/FADD2 and 196 us with LDS/STS -- the
+// persistent pipeline is latency- not issue-bound -- so both stay off here
+// (the LDG fused and pass kernels, which are issue-bound, use packed math).
+#ifdef SFFT_TMA_PACK
+constexpr bool TMA_PACK = true;
+#else
+constexpr bool TMA_PACK = false;
+#endif
+
 struct TmaArgs {
     int64_t ntiles;
     double scale;        // 1/N when the caller swapped the maps for the inverse
@@ -145,7 +156,13 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
     constexpr int N = Sh::N, R = Sh::R, P = Sh::P, S = Sh::S, LR = Sh::LR, NPASS = Sh::NPASS,
                   TILE = Sh::TILE, SSTR = Sh::SSTR, W = Sh::W;
     extern __shared__ unsigned char smem_raw[];
+    // 1024-byte alignment for the 128B swizzle (see TMA_PACK for why the
+    // generic-pointer form is the default)
+#ifndef SFFT_TMA_LDS
     unsigned char *smem = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+#else
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+#endif
     unsigned char *in_buf = smem + Sh::IN_OFF;      // [STAGES][2 planes][TILE]
     unsigned char *out_buf = smem + Sh::OUT_OFF;    // [OB][2][TILE]
     T *ex = reinterpret_cast<T *>(smem + Sh::EX_OFF);
@@ -177,7 +194,7 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
         for (int s = 0; s < STAGES && s < nk; ++s) issue_load(s, blockIdx.x + (int64_t)s * gridDim.x);
     }
 
-    T vr[R], vi[R];
+    vec2_t<T> v[R];
     // fp32: base factors of passes >= 1 depend only on the thread, not on
     // the tile -- fetch them once for the whole persistent loop
     constexpr bool PRE = PRE_T && FactorTw<T>::value;
@@ -225,18 +242,18 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
             {                                                                                        \
                 const int e = j + r * (N / RP);                                                      \
                 if (p == 0) {                                                                        \
-                    vr[u * RP + r] = lds_at<T>(inr, swz<T, N>(sl, e));                               \
-                    vi[u * RP + r] = lds_at<T>(ini, swz<T, N>(sl, e));                               \
+                    v[u * RP + r].x = lds_at<T>(inr, swz<T, N>(sl, e));                               \
+                    v[u * RP + r].y = lds_at<T>(ini, swz<T, N>(sl, e));                               \
                 } else {                                                                             \
-                    vr[u * RP + r] = exr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];                    \
-                    vi[u * RP + r] = exi[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];                    \
+                    v[u * RP + r].x = exr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];                    \
+                    v[u * RP + r].y = exi[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];                    \
                 }                                                                                    \
             }                                                                                        \
         }                                                                                            \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
         {                                                                                            \
             const int j = t + P * u;                                                                 \
-            dit_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (j & (ns - 1)), tw,              \
+            dit_stages<T, KP, true, TMA_PACK>(v + u * RP, sp, (j & (ns - 1)), tw,              \
                               (PRE && p > 0) ? &pre[p][u * KP] : nullptr);                       \
         }                                                                                            \
         if (p < NPASS - 1) {                                                                         \
@@ -248,8 +265,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                 _Pragma("unroll") for (int f = 0; f < RP; ++f)                                       \
                 {                                                                                    \
                     const int e = base + ns * f;                                                     \
-                    exr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = vr[u * RP + brev(f, KP)];              \
-                    exi[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = vi[u * RP + brev(f, KP)];              \
+                    exr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].x;              \
+                    exi[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].y;              \
                 }                                                                                    \
             }                                                                                        \
             if (p == 0) {                                                                            \
@@ -272,7 +289,7 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                 _Pragma("unroll") for (int f = 0; f < RP; ++f)                                       \
                 {                                                                                    \
                     const int e = j + ns * f;                                                        \
-                    T re = vr[u * RP + brev(f, KP)], im = vi[u * RP + brev(f, KP)];                  \
+                    T re = v[u * RP + brev(f, KP)].x, im = v[u * RP + brev(f, KP)].y;                  \
                     if (do_scale) { re *= scale; im *= scale; }                                      \
                     sts_at<T>(outr, swz<T, N>(sl, e), re);                                           \
                     sts_at<T>(outi, swz<T, N>(sl, e), im);                                           \
@@ -307,18 +324,18 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                 const int e = base + ns * f;                                                         \
                 const int d = u * RP + brev(f, KP);                                                  \
                 if (q == 0) {                                                                        \
-                    vr[d] = lds_at<T>(inr, swz<T, N>(sl, e));                                        \
-                    vi[d] = lds_at<T>(ini, swz<T, N>(sl, e));                                        \
+                    v[d].x = lds_at<T>(inr, swz<T, N>(sl, e));                                        \
+                    v[d].y = lds_at<T>(ini, swz<T, N>(sl, e));                                        \
                 } else {                                                                             \
-                    vr[d] = exr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];                                 \
-                    vi[d] = exi[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];                                 \
+                    v[d].x = exr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];                                 \
+                    v[d].y = exi[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];                                 \
                 }                                                                                    \
             }                                                                                        \
         }                                                                                            \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
         {                                                                                            \
             const int j = t + P * u;                                                                 \
-            dif_stages<T, KP>(vr + u * RP, vi + u * RP, sp, (j & (ns - 1)), tw,              \
+            dif_stages<T, KP, true, TMA_PACK>(v + u * RP, sp, (j & (ns - 1)), tw,              \
                               (PRE && p > 0) ? &pre[p][u * KP] : nullptr);                       \
         }                                                                                            \
         if (p > 0) {                                                                                 \
@@ -329,8 +346,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                 _Pragma("unroll") for (int r = 0; r < RP; ++r)                                       \
                 {                                                                                    \
                     const int e = j + r * (N / RP);                                                  \
-                    exr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = vr[u * RP + r];                    \
-                    exi[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = vi[u * RP + r];                    \
+                    exr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].x;                    \
+                    exi[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].y;                    \
                 }                                                                                    \
             }                                                                                        \
             if (q == 0) {                                                                            \
@@ -352,7 +369,7 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                 _Pragma("unroll") for (int r = 0; r < RP; ++r)                                       \
                 {                                                                                    \
                     const int e = j + r * (N / RP);                                                  \
-                    T re = vr[u * RP + r], im = vi[u * RP + r];                                      \
+                    T re = v[u * RP + r].x, im = v[u * RP + r].y;                                      \
                     if (do_scale) { re *= scale; im *= scale; }                                      \
                     sts_at<T>(outr, swz<T, N>(sl, e), re);                                           \
                     sts_at<T>(outi, swz<T, N>(sl, e), im);                                           \
