@@ -289,6 +289,8 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     const double scale = inv ? 1.0 / (double)(int64_t(1) << m) : 1.0;
 
     if (m <= kFusedMaxLog) {
+        if (batch > (int64_t(0x7fffffff) << (m <= 2 ? 8 - m : 0)) || (m > 2 && batch > 0x7fffffffLL))
+            return fail(SFFT_ECAPACITY, "batch %lld exceeds one launch (2^31 rows); split the batch", (long long)batch);
         const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
         const bool aligned = ((uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)y0 | (uintptr_t)y1) % 16 == 0 &&
                              ((size_t)is * esz) % 16 == 0 && ((size_t)os * esz) % 16 == 0 &&
@@ -421,6 +423,8 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
             continue;
         }
         const int64_t grid = batch * ((n >> gr.L) / TJ);
+        if (grid > 0x7fffffffLL)
+            return fail(SFFT_ECAPACITY, "batch %lld x N=2^%d exceeds one launch; split the batch", (long long)batch, m);
         cudaError_t e = fn(a, p->algo == SFFT_DIF, first && il, last && il, grid, st);
         if (e != cudaSuccess) return cuda_fail(e, "pass kernel launch");
     }

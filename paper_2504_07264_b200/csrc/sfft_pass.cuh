@@ -84,7 +84,11 @@ struct PassShape {
     static constexpr int P = SUB / R;                 // threads per sub-problem
     // sub-problems per CTA: 128-byte global runs (32 fp32 / 16 fp64), halved
     // for the 2^10-point groups so the [e][TJ+1] tile still fits one SM
+#ifdef SFFT_PASS_TJ64
+    static constexpr int TJ = (sizeof(T) == 4 ? (L <= 7 ? 64 : 32) : 16) >> (L >= 10 ? 1 : 0);
+#else
     static constexpr int TJ = (sizeof(T) == 4 ? 32 : 16) >> (L >= 10 ? 1 : 0);
+#endif
     static constexpr int NT = TJ * P;
     static constexpr int RS = TJ + 1;                 // smem row stride
     static constexpr int NPI = (L + LR - 1) / LR;     // internal register passes

@@ -7,7 +7,10 @@ IFS=';' read -ra VS <<< "${VARIANTS:-cur=}"
 for v in "${VS[@]}"; do
   name=${v%%=*}; flags=${v#*=}
   d=/tmp/ab_$name; rm -rf $d && cp -r "$GRAFT_REPO_ROOT" $d
-  make -C $d/paper_2504_07264_b200/csrc -B -j16 NVFLAGS="$NV $flags" > $d.log 2>&1 || { tail -5 $d.log; exit 1; }
+  # a "ENV:K=V" word in the flags is exported for the generator instead of passed to nvcc
+  envs=$(echo "$flags" | tr ' ' '\n' | grep '^ENV:' | sed 's/^ENV://' | tr '\n' ' ')
+  nvf=$(echo "$flags" | tr ' ' '\n' | grep -v '^ENV:' | tr '\n' ' ')
+  (cd $d/paper_2504_07264_b200/csrc && rm -f sfft_inst_*.cu && env $envs make -B -j16 NVFLAGS="$NV $nvf") > $d.log 2>&1 || { tail -5 $d.log; exit 1; }
   DIRS+=("$name:$d")
 done
 if [ -d "$GRAFT_REPO_ROOT/ab_old/csrc" ] && [ -n "$WITH_OLD" ]; then
