@@ -289,7 +289,7 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     const double scale = inv ? 1.0 / (double)(int64_t(1) << m) : 1.0;
 
     if (m <= kFusedMaxLog) {
-        if (batch > (int64_t(0x7fffffff) << (m <= 2 ? 8 - m : 0)) || (m > 2 && batch > 0x7fffffffLL))
+        if (batch > 0x7fffffffLL)
             return fail(SFFT_ECAPACITY, "batch %lld exceeds one launch (2^31 rows); split the batch", (long long)batch);
         const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
         const bool aligned = ((uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)y0 | (uintptr_t)y1) % 16 == 0 &&
