@@ -294,9 +294,16 @@ def run_ours(args):
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    # SFFT_BENCH_BACKEND=gloo (test hook): ranks may share a GPU (index
+    # local % device_count) and the barrier / max-over-ranks go over gloo
+    backend = os.environ.get("SFFT_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     device = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
     torch.cuda.set_device(device)
 
@@ -369,7 +376,7 @@ def run_ours(args):
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=device)
+        t = torch.tensor([v], dtype=torch.float64, device=device if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 

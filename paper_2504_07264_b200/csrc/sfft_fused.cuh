@@ -103,6 +103,9 @@ struct FusedShape {
     static constexpr int P = N / R;                       // threads per signal
     static constexpr int NT = P > 256 ? P : 256;          // threads per block
     static constexpr int S = NT / P;                      // signals per block
+#ifdef SFFT_FUSED_MINB
+    static constexpr int MINB = SFFT_FUSED_MINB * NT > 2048 ? 2048 / NT : SFFT_FUSED_MINB;
+#endif
     static constexpr int NPASS = LOGN == 0 ? 0 : (LOGN + LR - 1) / LR;
     template <typename T>
     static constexpr int sstr() { return LOGN == 0 ? 1 : ex_sstr<T, LOGN, LR, NT>(); }   // per-signal plane stride
@@ -269,7 +272,11 @@ __device__ __forceinline__ void dif_from(vec2_t<T> *v, int t, int64_t row, bool 
 // Whether that pays depends on the size (register pressure vs latency);
 // tools/tune.py measures both and gen_inst.py's AUTO table records the pick.
 template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL, bool PRE = false>
+#ifdef SFFT_FUSED_MINB
+__global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT, FusedShape<LOGN, LR_REQ>::MINB)
+#else
 __global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT)
+#endif
 sfft_fused_kernel(const FusedArgs a)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
