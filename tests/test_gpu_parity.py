@@ -47,7 +47,7 @@ def gpu_split(re, im, algo="dit", inverse=False, radix_log=0, kernel="auto", pre
 
 
 FUSED_M = list(range(0, 13))
-LARGE_M = [13, 14, 16, 17, 20]
+LARGE_M = [13, 14, 16, 17, 20, 22]
 
 
 @pytest.mark.parametrize("inverse", [False, True])
@@ -295,3 +295,29 @@ print("ok")
     env = dict(__import__('os').environ, SFFT_PASS_TMA="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("m", [6, 10, 14])
+def test_cuda_graph_capture_and_replay(cuda, m):
+    # exec is a pure stream-ordered launch sequence (no sync, no allocation
+    # in the C ABI), so it can be captured in a CUDA graph and replayed
+    rng = np.random.default_rng(12)
+    xr = torch.from_numpy(rng.standard_normal((64, 1 << m)).astype(np.float32)).cuda()
+    xi = torch.from_numpy(rng.standard_normal((64, 1 << m)).astype(np.float32)).cuda()
+    plan = sf.make_plan(m, dtype=torch.float32, device="cuda:0")
+    yr, yi = torch.empty_like(xr), torch.empty_like(xi)
+    sf.fft_split(xr, xi, out=(yr, yi), plan=plan)          # warm up outside the capture
+    want = (yr.clone(), yi.clone())
+    yr.zero_()
+    yi.zero_()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            sf.fft_split(xr, xi, out=(yr, yi), plan=plan)
+    torch.cuda.current_stream().wait_stream(s)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(yr, want[0]) and torch.equal(yi, want[1])
