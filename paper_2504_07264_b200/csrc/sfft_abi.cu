@@ -12,10 +12,15 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <atomic>
 #include <string>
 #include <thread>
 #include <utility>
+
+#ifndef SFFT_PASS_ASYNC_DEFAULT
+#define SFFT_PASS_ASYNC_DEFAULT 0
+#endif
 #include <vector>
 
 #include "../../include/splitfft_b200.h"
@@ -201,15 +206,24 @@ int upload_two_level(sfft_plan *p)
     std::vector<double> cr((size_t)hc), ci((size_t)hc), fr((size_t)hf), fi((size_t)hf);
     stage_table(CL, hc, cr.data(), ci.data());
     stage_table(m, hf, fr.data(), fi.data());
-    std::vector<double2> c2((size_t)hc), f2((size_t)hf);
+    // fine table, then the lane table: stage i's factors w_i(l), l < 32, at
+    // hf + (i-1)*32 + l (entries past 2^(i-1) are never read)
+    const int64_t nf = hf + 32 * (int64_t)m;
+    std::vector<double2> c2((size_t)hc), f2((size_t)nf, make_double2(0.0, 0.0));
     for (int64_t q = 0; q < hc; ++q) c2[q] = make_double2(cr[q], ci[q]);
     for (int64_t q = 0; q < hf; ++q) f2[q] = make_double2(fr[q], fi[q]);
+    for (int i = 1; i <= m; ++i) {
+        const int64_t hl = std::min<int64_t>(32, int64_t(1) << (i - 1));
+        std::vector<double> lr((size_t)hl), li((size_t)hl);
+        stage_table(i, hl, lr.data(), li.data());
+        for (int64_t l = 0; l < hl; ++l) f2[hf + 32 * (i - 1) + l] = make_double2(lr[l], li[l]);
+    }
     cudaError_t e = cudaMalloc(&p->d_coarse, sizeof(double2) * (size_t)hc);
-    if (e == cudaSuccess) e = cudaMalloc(&p->d_fine, sizeof(double2) * (size_t)hf);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_fine, sizeof(double2) * (size_t)nf);
     if (e == cudaSuccess)
         e = cudaMemcpy(p->d_coarse, c2.data(), sizeof(double2) * (size_t)hc, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
-        e = cudaMemcpy(p->d_fine, f2.data(), sizeof(double2) * (size_t)hf, cudaMemcpyHostToDevice);
+        e = cudaMemcpy(p->d_fine, f2.data(), sizeof(double2) * (size_t)nf, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return cuda_fail(e, "uploading two-level twiddles");
     p->coarse_log = CL;
     return SFFT_OK;
@@ -244,6 +258,14 @@ static bool pass_tma_enabled()
 {
     const char *e = getenv("SFFT_PASS_TMA");
     return e && atoi(e) != 0;
+}
+
+// The persistent cp.async-pipelined pass kernel (sfft_pass_async.cuh) for
+// the planar groups with S > 0.  SFFT_PASS_ASYNC=0/1 overrides the default.
+static bool pass_async_enabled()
+{
+    const char *e = getenv("SFFT_PASS_ASYNC");
+    return e ? atoi(e) != 0 : SFFT_PASS_ASYNC_DEFAULT;
 }
 
 std::vector<Group> split_groups(int m)
@@ -420,6 +442,13 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
             Lc.a.fine = a.fine;
             cudaError_t e = tf(Lc, st);
             if (e != cudaSuccess) return cuda_fail(e, "TMA pass kernel launch");
+            continue;
+        }
+        PassAsyncLaunchFn af = (pass_async_enabled() && gr.S > 0 && planar_here && p->kernel != SFFT_KERNEL_LDG)
+                                   ? pass_async_launcher(p->dtype, gr.L, p->algo == SFFT_DIF, false) : nullptr;
+        if (af) {
+            cudaError_t e = af(a, st);
+            if (e != cudaSuccess) return cuda_fail(e, "async pass kernel launch");
             continue;
         }
         const int64_t grid = batch * ((n >> gr.L) / TJ);
@@ -779,6 +808,12 @@ static int dist_exec(const sfft_dist_plan *d, int phase, const void *x_re, const
             a.jpos = L1 - b;
             a.in_map = {b, L1 - b, -1, m - b};
             a.out_map = {b, L1 - b, -1, m - b};
+        }
+        PassAsyncLaunchFn af = (pass_async_enabled() && gr.S > 0) ? pass_async_launcher(p->dtype, gr.L, false, true) : nullptr;
+        if (af) {
+            cudaError_t e = af(a, (cudaStream_t)stream);
+            if (e != cudaSuccess) return cuda_fail(e, "async pass kernel launch (sharded)");
+            continue;
         }
         const int64_t grid = ((n >> gr.L) >> b) / TJ;
         cudaError_t e = fn(a, false, false, false, grid, (cudaStream_t)stream);

@@ -74,7 +74,13 @@ __device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v);
 //   TwCatTop:   stage-major up to cat_top, then the stage-m table read with
 //               stride 2^(m-i) (fp64 plans with m > 20 only).
 //   TwTwoLevel: fp32 N > 4096: stage-major fp32 table up to cat_top (12);
-//               above it coarse[hi] * fine[lo] in fp64, rounded to fp32.
+//               above it w_i(q) = w_i(q & 31) * w_i(q & ~31), the first
+//               from a per-stage 32-entry "lane" table (the lanes of a warp
+//               hold consecutive q, so this read is contiguous), the second
+//               lane-uniform as coarse[hi] * fine[lo]; all in fp64, rounded
+//               to fp32 once.  (Reading w_m(q << (m-i)) directly made every
+//               lane of a warp touch its own sector: l1tex at 89% on the
+//               late N = 2^28 pass groups.)
 template <typename T>
 struct TwCat {
     using index_t = int;
@@ -101,25 +107,35 @@ struct TwCatTop {
 
 template <typename T>
 struct TwTwoLevel {
-    using index_t = int64_t;
+    using index_t = int64_t;   // (uint32_t indices measured slower: ptxas spills at 64 registers)
     const vec2_t<T> *tab;      // stage-major fp32, stages 1..cat_top
     int cat_top;
     const double2 *coarse;     // stage coarse_log factors, 2^(coarse_log-1) entries
     int coarse_log;
-    const double2 *fine;       // exp(-j 2 pi lo / 2^m), lo < 2^(m - coarse_log)
+    const double2 *fine;       // exp(-j 2 pi lo / 2^m), lo < 2^(m - coarse_log),
+                               // then the lane table: w_i(l) at (i-1)*32 + l, l < 32
     int m;
+    __device__ __forceinline__ void set_tables(const double2 *c, int clog, const double2 *f, int m_)
+    {
+        coarse = c;
+        coarse_log = clog;
+        fine = f;
+        m = m_;
+    }
     __device__ __forceinline__ vec2_t<T> get(int i, int64_t q) const
     {
         if (i <= cat_top) return ldtw(tab + ((int64_t(1) << (i - 1)) - 1) + q);
-        const int64_t qq = q << (m - i);
         const int fb = m - coarse_log;
+        const int64_t qq = (q >> 5) << (m - i + 5);          // w_m(qq) = w_i(q & ~31)
         const double2 a = __ldg(coarse + (qq >> fb));
         const double2 b = __ldg(fine + (qq & ((int64_t(1) << fb) - 1)));
-        double r, im;
+        const double2 l = __ldg(fine + (int64_t(1) << fb) + (i - 1) * 32 + (int)(q & 31));
+        double r, im, r2, im2;
         cmul(a.x, a.y, b.x, b.y, r, im);
+        cmul(r, im, l.x, l.y, r2, im2);
         vec2_t<T> w;
-        w.x = (T)r;
-        w.y = (T)im;
+        w.x = (T)r2;
+        w.y = (T)im2;
         return w;
     }
 };

@@ -23,6 +23,10 @@ using TmaLaunchFn = cudaError_t (*)(const TmaLaunch &L, cudaStream_t st);
 // Launch the TMA-pipelined pass kernel (groups with S > 0, planar rows).
 using PassTmaLaunchFn = cudaError_t (*)(const PassTmaLaunch &L, cudaStream_t st);
 
+// Launch the persistent cp.async-pipelined pass kernel (groups with S > 0,
+// planar rows); the launcher sizes the grid to the resident CTAs.
+using PassAsyncLaunchFn = cudaError_t (*)(const PassArgs &a, cudaStream_t st);
+
 constexpr int kFusedMaxLog = 12;
 constexpr int kMaxRadixLog = 5;
 constexpr int kPassMinL = 4, kPassMaxL = 10;
@@ -48,6 +52,10 @@ void auto_choice(int dtype, int logn, bool *tma, int *lr, bool *pre);  // kernel
 PassTmaLaunchFn pass_tma_launcher(int dtype, int L, bool dif);
 PassTmaLaunchFn pass_tma_launcher_f32(int L, bool dif);
 PassTmaLaunchFn pass_tma_launcher_f64(int L, bool dif);
+
+PassAsyncLaunchFn pass_async_launcher(int dtype, int L, bool dif, bool dist);
+PassAsyncLaunchFn pass_async_launcher_f32(int L, bool dif, bool dist);
+PassAsyncLaunchFn pass_async_launcher_f64(int L, bool dif, bool dist);
 
 void count_launch();
 

@@ -167,10 +167,7 @@ __device__ __forceinline__ typename PassTw<T, S0>::type make_pass_tw(const PassA
             tw.top_tab = (const vec2_t<T> *)a.tw_top_tab;
             tw.top = a.m;
         } else {
-            tw.coarse = a.coarse;
-            tw.coarse_log = a.coarse_log;
-            tw.fine = a.fine;
-            tw.m = a.m;
+            tw.set_tables(a.coarse, a.coarse_log, a.fine, a.m);
         }
     }
     return tw;
@@ -178,8 +175,13 @@ __device__ __forceinline__ typename PassTw<T, S0>::type make_pass_tw(const PassA
 
 // (plain __launch_bounds__(NT): an explicit min-blocks of 1, 5 or 6 measured
 // 20%, 4% and 50% slower on N = 2^28, tools/ab_variants.sh)
+#ifdef SFFT_PASS_MINB
+#define SFFT_PASS_LB(T, L, LR) __launch_bounds__(PassShape<T, L, LR>::NT, SFFT_PASS_MINB)
+#else
+#define SFFT_PASS_LB(T, L, LR) __launch_bounds__(PassShape<T, L, LR>::NT)
+#endif
 template <typename T, int L, int LR_REQ, bool DIF, bool IL_IN, bool IL_OUT, bool S0, bool DIST>
-__global__ void __launch_bounds__(PassShape<T, L, LR_REQ>::NT)
+__global__ void SFFT_PASS_LB(T, L, LR_REQ)
 sfft_pass_kernel(const PassArgs a)
 {
     using Sh = PassShape<T, L, LR_REQ>;
@@ -253,6 +255,31 @@ sfft_pass_kernel(const PassArgs a)
     constexpr bool PRE = false;
 #endif
     vec2_t<T> pre[NPI][R];
+    // fp32 groups after the first, -DSFFT_PASS_PRE0: only the base factors of
+    // the first internal pass are fetched up front, before the tile's loads are
+    // issued, so their latency overlaps the data's (fetched inside the pass
+    // they were issued only after the loads landed: ncu showed the warps
+    // waiting on one scoreboard for both)
+    // (measured slower on N = 2^28: 76 registers, 3 CTAs per SM; opt-in)
+#ifdef SFFT_PASS_PRE0
+    constexpr bool PRE0 = FactorTw<T>::value && !S0 && !PRE;
+#else
+    constexpr bool PRE0 = false;
+#endif
+    constexpr int PP0 = DIF ? NPI - 1 : 0;   // the first internal pass
+    vec2_t<T> pre0[R];
+    if constexpr (PRE0) {
+        const int sp = PP0 * LR;
+        const int kp = cmin(LR, L - sp);
+        const int nsp = 1 << sp;
+#pragma unroll
+        for (int u = 0; u < R / (1 << kp); ++u) {
+            const int jp = t + P * u;
+            const I cb = (I)(c + ((uint32_t)(jp & (nsp - 1)) << S));
+#pragma unroll
+            for (int tt = 1; tt <= kp; ++tt) pre0[u * kp + tt - 1] = tw.get(S + sp + tt, cb);
+        }
+    }
     if constexpr (PRE) {
 #pragma unroll
         for (int pp = 0; pp < NPI; ++pp) {
@@ -297,7 +324,7 @@ sfft_pass_kernel(const PassArgs a)
             const int jp = t + P * u;                                                           \
             dit_stages<T, KP, S0>(v + u * RP, S + sp,                             \
                                   (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw,               \
-                                  PRE ? &pre[pp][u * KP] : nullptr);                            \
+                                  PRE ? &pre[pp][u * KP] : (PRE0 && pp == PP0) ? &pre0[u * KP] : nullptr);                            \
         }                                                                                       \
         const bool last = pp == NPI - 1;                                                        \
         if (!last || S0) {                                                                      \
@@ -386,7 +413,7 @@ sfft_pass_kernel(const PassArgs a)
             const int jp = t + P * u;                                                           \
             dif_stages<T, KP, S0>(v + u * RP, S + sp,                             \
                                   (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw,               \
-                                  PRE ? &pre[pp][u * KP] : nullptr);                            \
+                                  PRE ? &pre[pp][u * KP] : (PRE0 && pp == PP0) ? &pre0[u * KP] : nullptr);                            \
         }                                                                                       \
         if (pp != 0) {                                                                          \
             if (!first || S0) __syncthreads();                                                  \

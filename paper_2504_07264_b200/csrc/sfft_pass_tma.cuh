@@ -73,10 +73,7 @@ __device__ __forceinline__ typename PassTw<T, false>::type make_tma_pass_tw(cons
         tw.top_tab = (const vec2_t<T> *)a.tw_top_tab;
         tw.top = a.m;
     } else {
-        tw.coarse = a.coarse;
-        tw.coarse_log = a.coarse_log;
-        tw.fine = a.fine;
-        tw.m = a.m;
+        tw.set_tables(a.coarse, a.coarse_log, a.fine, a.m);
     }
     return tw;
 }

@@ -266,11 +266,18 @@ def test_host_pipeline_many_chunks(cuda, monkeypatch, pinned):
         assert torch.equal(out_r, dr.cpu()) and torch.equal(out_i, di.cpu())
 
 
+PASS_VARIANTS = {"tma": {"SFFT_PASS_TMA": "1"}, "async": {"SFFT_PASS_ASYNC": "1"},
+                 "plain": {"SFFT_PASS_ASYNC": "0"}}
+
+
+@pytest.mark.parametrize("variant", sorted(PASS_VARIANTS))
 @pytest.mark.parametrize("algo", ["dit", "dif"])
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("m", [13, 16, 20])
-def test_tma_pass_kernel_opt_in(cuda, m, dtype, algo):
-    # the TMA-pipelined pass kernel (opt-in, SFFT_PASS_TMA=1) in a subprocess
+def test_pass_kernel_variants(cuda, m, dtype, algo, variant):
+    # each pass-kernel family for the groups with S > 0, forced through its
+    # environment switch in a subprocess: the TMA-pipelined kernel (opt-in),
+    # the persistent cp.async kernel and the plain LDG pass kernel
     import subprocess
     import sys
     code = f"""
@@ -292,7 +299,7 @@ for inv in (False, True):
         assert err <= 1e-5 * {m}, err
 print("ok")
 """
-    env = dict(__import__('os').environ, SFFT_PASS_TMA="1")
+    env = dict(__import__('os').environ, **PASS_VARIANTS[variant])
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
 
