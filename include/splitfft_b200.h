@@ -95,6 +95,16 @@ int sfft_plan_info(const sfft_plan *plan, int *log2n, int *dtype,
                    int *algorithm, int *device, int *launches_per_exec,
                    int *log2_radix, int *kernel);
 
+/* The launch schedule exec uses for `batch` rows (interleaved != 0: the
+ * interleaved layout): kernel launches per exec, and HBM sweeps per exec --
+ * passes that read and write the whole signal once.  One launch per sweep,
+ * except the opt-in (environment SFFT_BLOCKED=1) L2-blocked schedule of one
+ * long DIT transform (batch 1, planar, log2n >= 23): two sweeps (a four-step split, block by block with the
+ * intermediate of each block kept in L2) of many launches.  No reference
+ * analogue (introspection, used for the roofline unit). */
+int sfft_exec_schedule(const sfft_plan *plan, int64_t batch, int interleaved,
+                       int *launches, int *sweeps);
+
 /* Bytes of device workspace exec needs for `batch` rows (0 for the fused
  * single-kernel path, log2n <= 12). */
 int sfft_workspace_bytes(const sfft_plan *plan, int64_t batch, size_t *bytes);

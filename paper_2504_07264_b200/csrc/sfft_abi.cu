@@ -18,6 +18,9 @@
 #include <thread>
 #include <utility>
 
+#ifndef SFFT_BLOCK_MIN_M_DEFAULT
+#define SFFT_BLOCK_MIN_M_DEFAULT 23
+#endif
 #ifndef SFFT_PASS_ASYNC_DEFAULT
 #define SFFT_PASS_ASYNC_DEFAULT 0
 #endif
@@ -149,6 +152,10 @@ struct sfft_plan {
     int coarse_log = 0;
     double2 *d_fine = nullptr;
     std::vector<Group> groups;
+    // L2-blocked schedule: worker streams, created on first use
+    static constexpr int kWorkers = 4;
+    cudaStream_t wst[kWorkers] = {};
+    std::mutex wmu;
 };
 
 namespace {
@@ -236,6 +243,8 @@ void free_plan(sfft_plan *p)
     if (p->d_top) cudaFree(p->d_top);
     if (p->d_coarse) cudaFree(p->d_coarse);
     if (p->d_fine) cudaFree(p->d_fine);
+    for (cudaStream_t w : p->wst)
+        if (w) cudaStreamDestroy(w);
     delete p;
 }
 
@@ -248,6 +257,72 @@ static int pass_max_l()
     const char *e = getenv("SFFT_PASS_MAX_L");
     int v = e ? atoi(e) : 8;
     return v < kPassMinL ? kPassMinL : (v > kPassMaxL ? kPassMaxL : v);
+}
+
+// Groups of at most pass_max_l() stages covering `stages` consecutive stages
+// from S0 (balanced, each >= kPassMinL when stages allows).
+static std::vector<Group> split_range(int S0, int stages)
+{
+    const int maxl = pass_max_l();
+    const int G = (stages + maxl - 1) / maxl;
+    std::vector<Group> g;
+    int S = S0;
+    for (int k = 0; k < G; ++k) {
+        const int L = stages / G + (k < stages % G ? 1 : 0);
+        g.push_back({S, L});
+        S += L;
+    }
+    return g;
+}
+
+// L2-blocked schedule for one long DIT transform (batch 1, planar), the
+// four-step split done inside one GPU: phase A runs stages 1..TA (TA =
+// floor(m/2)) column block by column block, phase B stages TA+1..m block by
+// block of the low TA index bits.  Inside a phase, consecutive launches of
+// one block hand over a block-sized scratch that stays in L2 (the 126 MB L2
+// holds a 32 MB block), so HBM sees two sweeps over the signal instead of
+// one per group.  The tile enumeration and the scratch addressing are the
+// sharded transform's (sfft_dist_*): the block id is a field of the
+// sub-problem index (jb bits at jpos) that the scratch maps squeeze out.
+struct Blocked {
+    bool on = false;
+    int TA = 0, bA = 0, bB = 0;   // phase split; log2 (columns | low-index values) per block
+    std::vector<Group> ga, gb;
+};
+
+static Blocked blocked_schedule(const sfft_plan *p, int64_t batch, bool il)
+{
+    Blocked b;
+    const int m = p->log2n;
+    if (il || batch != 1 || p->algo != SFFT_DIT || m <= kFusedMaxLog) return b;
+    // opt-in (SFFT_BLOCKED=1): measured slower on N = 2^28 fp32 (4.6 ms with
+    // 4 worker streams, 6.1 ms on one stream, vs 3.6 ms for the 4-sweep
+    // schedule): a 32 MB block launch is too short to reach steady state,
+    // and the pass kernel is closer to issue-bound than HBM-bound
+    const char *e = getenv("SFFT_BLOCKED");
+    if (!e || atoi(e) == 0) return b;
+    const char *mm = getenv("SFFT_BLOCK_MIN_M");
+    if (m < (mm ? atoi(mm) : SFFT_BLOCK_MIN_M_DEFAULT)) return b;
+    b.TA = m / 2;
+    b.ga = split_range(0, b.TA);
+    b.gb = split_range(b.TA, m - b.TA);
+    if (b.ga.size() < 2 || b.gb.size() < 2) return b;   // one launch per phase: nothing to hand over
+    // complex elements per block: 2^22 fp32 / 2^21 fp64 (32 MB per block)
+    const char *bl = getenv("SFFT_BLOCK_LOG");
+    const int target = bl ? atoi(bl) : (p->dtype == SFFT_F32 ? 22 : 21);
+    // 5 <= b (a tile's 32 sub-problems stay contiguous), jb = TA - b >= 3
+    // (4 worker streams x 2 scratch slots fit the workspace)
+    auto clampb = [&](int v) { return v < 5 ? 5 : (v > b.TA - 3 ? b.TA - 3 : v); };
+    b.bA = clampb(target - (m - b.TA));
+    b.bB = clampb(target - (m - b.TA));
+    b.on = true;
+    return b;
+}
+
+static bool l2_discard_enabled()
+{
+    const char *e = getenv("SFFT_L2_DISCARD");
+    return e ? atoi(e) != 0 : true;
 }
 
 // The TMA-pipelined pass kernel (sfft_pass_tma.cuh) is correct (parity tests
@@ -294,6 +369,105 @@ int validate_exec(const sfft_plan *p, int64_t batch, int64_t is, int64_t os, int
         return fail(SFFT_EINVAL, "direction must be -1 (forward) or +1 (inverse), got %d", direction);
     if (batch > (int64_t(1) << 40)) return fail(SFFT_ECAPACITY, "batch %lld exceeds the launch limit", (long long)batch);
     return SFFT_OK;
+}
+
+int exec_blocked(const sfft_plan *pc, const Blocked &bp, const void *x0, const void *x1, void *y0, void *y1,
+                 bool inv, double scale, void *workspace, cudaStream_t st)
+{
+    sfft_plan *p = const_cast<sfft_plan *>(pc);   // worker streams only
+    const int m = p->log2n;
+    const int64_t n = int64_t(1) << m;
+    const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
+    const int jbA = bp.TA - bp.bA, jbB = bp.TA - bp.bB;
+    constexpr int NW = sfft_plan::kWorkers;
+    // blocks run on NW worker streams (block R on stream R % NW), so that the
+    // launches of different blocks overlap; workspace: the phase A -> B
+    // intermediate (2 planes of N), then per worker two scratch slots of 2
+    // planes (each <= N / (2 NW): jb >= 1 + log2 NW)
+    char *ws = (char *)workspace;
+    void *X[2] = {ws, ws + n * esz};
+    const size_t blk = (size_t)(n >> (jbA < jbB ? jbA : jbB)) * esz;
+    char *sb = ws + 2 * n * esz;
+    const bool disc = l2_discard_enabled();
+    std::lock_guard<std::mutex> lk(p->wmu);
+    for (int w = 0; w < NW; ++w)
+        if (!p->wst[w]) {
+            cudaError_t e = cudaStreamCreateWithFlags(&p->wst[w], cudaStreamNonBlocking);
+            if (e != cudaSuccess) return cuda_fail(e, "creating worker streams");
+        }
+    cudaEvent_t ev[NW + 1];
+    for (int w = 0; w <= NW; ++w) {
+        cudaError_t e = cudaEventCreateWithFlags(&ev[w], cudaEventDisableTiming);
+        if (e != cudaSuccess) return cuda_fail(e, "creating events");
+    }
+    int rc = SFFT_OK;
+    for (int ph = 0; ph < 2 && rc == SFFT_OK; ++ph) {
+        const std::vector<Group> &g = ph ? bp.gb : bp.ga;
+        const int jb = ph ? jbB : jbA, bl = ph ? bp.bB : bp.bA;
+        const int G = (int)g.size();
+        const int nw = (1 << jb) < NW ? (1 << jb) : NW;
+        cudaEventRecord(ev[NW], st);   // fork
+        for (int w = 0; w < nw; ++w) cudaStreamWaitEvent(p->wst[w], ev[NW], 0);
+        for (int R = 0; R < (1 << jb) && rc == SFFT_OK; ++R) {
+            const int w = R % nw;
+            char *slot[2] = {sb + (size_t)w * 4 * blk, sb + (size_t)w * 4 * blk + 2 * blk};
+            for (int i = 0; i < G; ++i) {
+                const Group gr = g[i];
+                const bool first = i == 0, last = i == G - 1;
+                PassLaunchFn fn = pass_launcher(p->dtype, gr.L);
+                if (!fn) {
+                    rc = fail(SFFT_EINVAL, "no pass kernel for L=%d", gr.L);
+                    break;
+                }
+                PassArgs a;
+                memset(&a, 0, sizeof a);
+                char *src = slot[(i + 1) % 2], *dst = slot[i % 2];
+                a.x0 = first ? (ph ? X[0] : x0) : src;
+                a.x1 = first ? (ph ? X[1] : x1) : src + blk;
+                a.y0 = last ? (ph ? y0 : X[0]) : dst;
+                a.y1 = last ? (ph ? y1 : X[1]) : dst + blk;
+                a.batch = 1;
+                a.in_stride = a.out_stride = n;
+                a.m = m;
+                a.S = gr.S;
+                a.swap_in = ph == 0 && first && inv;
+                a.swap_out = ph == 1 && last && inv;
+                a.scale = (ph == 1 && last) ? scale : 1.0;
+                a.tw = p->d_tw;
+                a.tw_cat_top = p->cat_top;
+                a.tw_top_tab = p->d_top;
+                a.coarse = p->d_coarse;
+                a.coarse_log = p->coarse_log;
+                a.fine = p->d_fine;
+                a.jb = jb;
+                a.jrank = R;
+                const AddrMap id = {0, 0, -1, m};
+                if (ph == 0) {   // block field: bits [S + bl, S + TA) of the sub-problem index
+                    a.jpos = gr.S + bl;
+                    a.in_map = first ? id : AddrMap{jb, gr.S + bl, -1, m - jb};
+                    a.out_map = last ? id : AddrMap{jb, gr.S + gr.L + bl, -1, m - jb};
+                } else {         // block field: bits [bl, TA) of the low index
+                    a.jpos = bl;
+                    a.in_map = first ? id : AddrMap{jb, bl, -1, m - jb};
+                    a.out_map = last ? id : AddrMap{jb, bl, -1, m - jb};
+                }
+                a.keep_out = !last;
+                a.discard_in = !first && disc;
+                const int64_t grid = ((n >> gr.L) >> jb) / pass_tile(p->dtype, gr.L);
+                cudaError_t e = fn(a, false, false, false, grid, p->wst[w]);
+                if (e != cudaSuccess) {
+                    rc = cuda_fail(e, "pass kernel launch (blocked)");
+                    break;
+                }
+            }
+        }
+        for (int w = 0; w < nw; ++w) {   // join
+            cudaEventRecord(ev[w], p->wst[w]);
+            cudaStreamWaitEvent(st, ev[w], 0);
+        }
+    }
+    for (int w = 0; w <= NW; ++w) cudaEventDestroy(ev[w]);
+    return rc;
 }
 
 int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, void *y1, bool il,
@@ -361,6 +535,10 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
 
     // multi-launch schedule: groups in order (DIT) or reverse order (DIF)
     if (!workspace) return fail(SFFT_EINVAL, "log2n=%d needs a workspace (sfft_workspace_bytes)", m);
+    {
+        const Blocked bp = blocked_schedule(p, batch, il);
+        if (bp.on) return exec_blocked(p, bp, x0, x1, y0, y1, inv, scale, workspace, st);
+    }
     const int64_t n = int64_t(1) << m;
     const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
     const int G = (int)p->groups.size();
@@ -602,6 +780,26 @@ int sfft_plan_info(const sfft_plan *p, int *log2n, int *dtype, int *algorithm, i
     return SFFT_OK;
 }
 
+int sfft_exec_schedule(const sfft_plan *p, int64_t batch, int interleaved, int *launches, int *sweeps)
+{
+    if (!p) return fail(SFFT_EINVAL, "plan is NULL");
+    if (batch < 0) return fail(SFFT_EINVAL, "batch must be >= 0, got %lld", (long long)batch);
+    int nl = 1, ns = 1;
+    if (p->log2n > kFusedMaxLog) {
+        const Blocked bp = blocked_schedule(p, batch, interleaved != 0);
+        if (bp.on) {
+            nl = (int)bp.ga.size() << (bp.TA - bp.bA);
+            nl += (int)bp.gb.size() << (bp.TA - bp.bB);
+            ns = 2;
+        } else {
+            nl = ns = (int)p->groups.size();
+        }
+    }
+    if (launches) *launches = nl;
+    if (sweeps) *sweeps = ns;
+    return SFFT_OK;
+}
+
 int sfft_workspace_bytes(const sfft_plan *p, int64_t batch, size_t *bytes)
 {
     if (!p) return fail(SFFT_EINVAL, "plan is NULL");
@@ -637,22 +835,8 @@ int sfft_exec_interleaved(const sfft_plan *plan, const void *x, void *y, int64_t
 struct sfft_dist_plan {
     sfft_plan *base = nullptr;   // tables of the full-size plan
     int nranks = 1, rank = 0, logg = 0, L1 = 0;
-    std::vector<Group> ga, gb;   // phase 0: stages 1..L1, phase 1: L1+1..m
+    std::vector<Group> ga, gb;   // phase 0: stages 1..L1, phase 1: L1+1..m (split_range)
 };
-
-static std::vector<Group> split_range(int S0, int L)
-{
-    const int maxl = pass_max_l();
-    const int G = (L + maxl - 1) / maxl;
-    std::vector<Group> g;
-    int S = S0;
-    for (int k = 0; k < G; ++k) {
-        int l = L / G + (k < L % G ? 1 : 0);
-        g.push_back({S, l});
-        S += l;
-    }
-    return g;
-}
 
 int sfft_dist_plan_create(int log2n, int dtype, int nranks, int rank, int device, sfft_dist_plan **out)
 {

@@ -74,7 +74,19 @@ struct PassArgs {
     int npeers;
     int seg_log;
     void *peer_re[8], *peer_im[8];
+    // L2-blocked schedule (sfft_abi.cu exec_blocked; DIST launches only):
+    // keep_out -- the destination is a block scratch the next launch reads
+    // back, store with the default (L2-resident) policy instead of
+    // evict-first; discard_in -- the source is such a scratch, drop its lines
+    // from L2 after reading them (discard.global.L2: no write-back of data
+    // that is dead)
+    int keep_out, discard_in;
 };
+
+__device__ __forceinline__ void l2_discard(const void *p)
+{
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 
 template <typename T, int L, int LR_REQ>
 struct PassShape {
@@ -234,6 +246,13 @@ sfft_pass_kernel(const PassArgs a)
                 return;
             }
         }
+        if constexpr (DIST && !IL_OUT) {
+            if (a.keep_out) {   // block scratch: leave it in L2 for the next launch
+                dst.br[off] = re;
+                dst.bi[off] = im;
+                return;
+            }
+        }
         dst.store(off, re, im);
     };
     auto get_in = [&](int64_t off, T &re, T &im) {
@@ -241,6 +260,25 @@ sfft_pass_kernel(const PassArgs a)
         src.load(off, x, y);
         re = swap_in ? y : x;
         im = swap_in ? x : y;
+    };
+    // after the first internal pass consumed the tile (so every load of it
+    // has landed): drop the scratch lines it came from.  A line is the TJ
+    // sub-problems of one element row e (128 bytes); the first thread of each
+    // row group issues the discards for its rows.
+    auto discard_tile = [&]() {
+        if constexpr (DIST && !DIF && !IL_IN) {
+            if (a.discard_in && jl == 0) {
+#pragma unroll
+                for (int u = 0; u < R / (1 << LR); ++u)
+#pragma unroll
+                    for (int r = 0; r < (1 << LR); ++r) {
+                        const int e = (t + P * u) + r * (SUB >> LR);
+                        const int64_t off = iaddr(j0 + (uint32_t)e * NJ);
+                        l2_discard(src.ar + off);
+                        l2_discard(src.ai + off);
+                    }
+            }
+        }
     };
 
     vec2_t<T> v[R];
@@ -326,6 +364,7 @@ sfft_pass_kernel(const PassArgs a)
                                   (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw,               \
                                   PRE ? &pre[pp][u * KP] : (PRE0 && pp == PP0) ? &pre0[u * KP] : nullptr);                            \
         }                                                                                       \
+        if (DIST && pp == 0) discard_tile();                                                    \
         const bool last = pp == NPI - 1;                                                        \
         if (!last || S0) {                                                                      \
             if (pp > 0) __syncthreads();                                                        \

@@ -98,6 +98,13 @@ class FftPlan:
     def launches_per_exec(self) -> int:
         return self._info()[4]
 
+    def schedule(self, batch: int = 1, interleaved: bool = False):
+        """(kernel launches, HBM sweeps) one exec of `batch` rows uses."""
+        nl, ns = ctypes.c_int(), ctypes.c_int()
+        _ffi.check(_ffi.lib.sfft_exec_schedule(self._handle, int(batch), int(bool(interleaved)),
+                                               ctypes.byref(nl), ctypes.byref(ns)))
+        return nl.value, ns.value
+
     @property
     def radix_log(self) -> int:
         return self._info()[5]

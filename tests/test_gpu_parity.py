@@ -328,3 +328,48 @@ def test_cuda_graph_capture_and_replay(cuda, m):
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(yr, want[0]) and torch.equal(yi, want[1])
+
+
+@pytest.mark.parametrize("discard", ["1", "0"])
+@pytest.mark.parametrize("m,block_log", [(18, 12), (20, 13), (22, 14), (23, 21)])
+def test_l2_blocked_schedule_f64_bitwise(cuda, monkeypatch, m, block_log, discard):
+    # the L2-blocked long-transform schedule (sfft_abi.cu exec_blocked),
+    # forced at small sizes with small blocks: still bitwise the reference's
+    # fp64 results, forward and inverse, with and without the L2 discards
+    monkeypatch.setenv("SFFT_BLOCKED", "1")
+    monkeypatch.setenv("SFFT_BLOCK_MIN_M", "13")
+    monkeypatch.setenv("SFFT_BLOCK_LOG", str(block_log))
+    monkeypatch.setenv("SFFT_L2_DISCARD", discard)
+    plan = sf.make_plan(m, dtype=torch.float64, device="cuda:0")
+    nl, ns = plan.schedule(1)
+    assert ns == 2 and nl > 4
+    assert plan.schedule(2) == (plan.launches_per_exec, plan.launches_per_exec)   # batch > 1: unblocked
+    rng = np.random.default_rng(m)
+    re = rng.standard_normal((1, 1 << m))
+    im = rng.standard_normal((1, 1 << m))
+    for inv in (False, True):
+        yr, yi = sf.fft_split(torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda(), plan=plan, inverse=inv)
+        wr, wi = oracle.fft_split_c(re, im, "dit", inv)
+        assert np.array_equal(bits(yr.cpu().numpy()), bits(wr)) and np.array_equal(bits(yi.cpu().numpy()), bits(wi))
+
+
+@pytest.mark.parametrize("m", [23, 24])
+def test_l2_blocked_schedule_f32(cuda, monkeypatch, m):
+    # fp32 at its intended sizes: against the oracle and the 4-sweep schedule
+    plan = sf.make_plan(m, dtype=torch.float32, device="cuda:0")
+    rng = np.random.default_rng(m + 1)
+    re = rng.standard_normal((1, 1 << m)).astype(np.float32)
+    im = rng.standard_normal((1, 1 << m)).astype(np.float32)
+    xr, xi = torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda()
+    ur, ui = sf.fft_split(xr, xi, plan=plan)
+    assert plan.schedule(1)[1] == plan.launches_per_exec
+    monkeypatch.setenv("SFFT_BLOCKED", "1")
+    assert plan.schedule(1)[1] == 2
+    yr, yi = sf.fft_split(xr, xi, plan=plan)
+    wr, wi = oracle.fft_split_c(re, im)
+    gr, gi = yr.cpu().numpy().astype(np.float64), yi.cpu().numpy().astype(np.float64)
+    err = np.sqrt(np.sum((gr - wr) ** 2 + (gi - wi) ** 2) / np.sum(wr ** 2 + wi ** 2))
+    assert err <= 1e-5 * m
+    num = torch.sqrt(torch.sum((yr - ur).double() ** 2 + (yi - ui).double() ** 2))
+    den = torch.sqrt(torch.sum(ur.double() ** 2 + ui.double() ** 2))
+    assert (num / den).item() <= 1e-6
