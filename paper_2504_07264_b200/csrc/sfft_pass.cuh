@@ -224,25 +224,46 @@ sfft_pass_kernel(const PassArgs a)
     auto iaddr = [&](uint32_t x) -> int64_t { return ioff + (DIST ? imap(x) : x); };
     auto oaddr = [&](uint32_t x) -> int64_t { return ooff + (DIST ? omap(x) : x); };
 
-    const PIO<T, IL_IN> src = make_pio<T, IL_IN>(a);
-    const PIO<T, IL_OUT> dst = make_pio<T, IL_OUT>(a);
+    PIO<T, IL_IN> src = make_pio<T, IL_IN>(a);
+    PIO<T, IL_OUT> dst = make_pio<T, IL_OUT>(a);
     const auto tw = make_pass_tw<T, S0>(a);
     using I = typename PassTw<T, S0>::type::index_t;
     const bool swap_in = a.swap_in != 0, swap_out = a.swap_out != 0;
     const T scale = (T)a.scale;
+    // the inverse's channel swap: planar sides exchange their plane pointers
+    // once (no per-element selects); interleaved sides swap values
+    if constexpr (!IL_IN) {
+        if (swap_in) {
+            const T *t0 = src.ar;
+            src.ar = src.ai;
+            src.ai = t0;
+        }
+    }
+    if constexpr (!IL_OUT) {
+        if (swap_out) {
+            T *t0 = dst.br;
+            dst.br = dst.bi;
+            dst.bi = t0;
+        }
+    }
 
     auto put_out = [&](int64_t off, T re, T im) {
         if (swap_out) {
-            const T t = re;
-            re = im * scale;
-            im = t * scale;
+            if constexpr (IL_OUT) {
+                const T t = re;
+                re = im * scale;
+                im = t * scale;
+            } else {   // planes already exchanged
+                re *= scale;
+                im *= scale;
+            }
         }
         if constexpr (DIST) {
             if (a.npeers > 0) {   // NVLink/NVSwitch peer store into the receiver's slot
                 const int h = (int)(off >> a.seg_log);
                 const int64_t r = ((int64_t)a.jrank << a.seg_log) + (off & ((int64_t(1) << a.seg_log) - 1));
-                st_stream((T *)a.peer_re[h] + r, re);
-                st_stream((T *)a.peer_im[h] + r, im);
+                st_stream((T *)(swap_out ? a.peer_im[h] : a.peer_re[h]) + r, re);
+                st_stream((T *)(swap_out ? a.peer_re[h] : a.peer_im[h]) + r, im);
                 return;
             }
         }
@@ -258,8 +279,13 @@ sfft_pass_kernel(const PassArgs a)
     auto get_in = [&](int64_t off, T &re, T &im) {
         T x, y;
         src.load(off, x, y);
-        re = swap_in ? y : x;
-        im = swap_in ? x : y;
+        if constexpr (IL_IN) {
+            re = swap_in ? y : x;
+            im = swap_in ? x : y;
+        } else {
+            re = x;
+            im = y;
+        }
     };
     // after the first internal pass consumed the tile (so every load of it
     // has landed): drop the scratch lines it came from.  A line is the TJ
