@@ -104,7 +104,8 @@ struct PassShape {
     static constexpr int NT = TJ * P;
     static constexpr int RS = TJ + 1;                 // smem row stride
     static constexpr int NPI = (L + LR - 1) / LR;     // internal register passes
-    static constexpr int smem_bytes() { return 2 * SUB * RS * (int)sizeof(T); }
+    // + the per-tile stage factors w_{S+s}(c), s = 1..L, of the TJ columns
+    static constexpr int smem_bytes() { return 2 * SUB * RS * (int)sizeof(T) + L * TJ * 2 * (int)sizeof(T); }
 };
 
 template <typename T, bool IL>
@@ -187,10 +188,20 @@ __device__ __forceinline__ typename PassTw<T, S0>::type make_pass_tw(const PassA
 
 // (plain __launch_bounds__(NT): an explicit min-blocks of 1, 5 or 6 measured
 // 20%, 4% and 50% slower on N = 2^28, tools/ab_variants.sh)
+// fp32: at least 1024 threads' worth of CTAs per SM (<= 64 registers; the
+// column-factor staging otherwise lands at 72-80 registers, 3 CTAs of 256
+// per SM, measured 3-4% slower on N = 2^28 even though the cap spills 20
+// bytes).  fp64: 0 = no minimum (the compiler's choice; 1 would let it take
+// up to 233 registers).
+template <typename T, int L, int LR>
+struct PassMinBlocks {
+    static constexpr int NT = PassShape<T, L, LR>::NT;
+    static constexpr int value = sizeof(T) == 4 ? (1024 / NT < 1 ? 1 : (1024 / NT > 8 ? 8 : 1024 / NT)) : 0;
+};
 #ifdef SFFT_PASS_MINB
 #define SFFT_PASS_LB(T, L, LR) __launch_bounds__(PassShape<T, L, LR>::NT, SFFT_PASS_MINB)
 #else
-#define SFFT_PASS_LB(T, L, LR) __launch_bounds__(PassShape<T, L, LR>::NT)
+#define SFFT_PASS_LB(T, L, LR) __launch_bounds__(PassShape<T, L, LR>::NT, (PassMinBlocks<T, L, LR>::value))
 #endif
 template <typename T, int L, int LR_REQ, bool DIF, bool IL_IN, bool IL_OUT, bool S0, bool DIST>
 __global__ void SFFT_PASS_LB(T, L, LR_REQ)
@@ -202,6 +213,7 @@ sfft_pass_kernel(const PassArgs a)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T *sr = reinterpret_cast<T *>(smem_raw);
     T *si = sr + SUB * RS;
+    vec2_t<T> *cs = reinterpret_cast<vec2_t<T> *>(si + SUB * RS);   // [L][TJ] column factors
 
     const int m = a.m;
     const int S = S0 ? 0 : a.S;
@@ -319,31 +331,41 @@ sfft_pass_kernel(const PassArgs a)
     constexpr bool PRE = false;
 #endif
     vec2_t<T> pre[NPI][R];
-    // fp32 groups after the first, -DSFFT_PASS_PRE0: only the base factors of
-    // the first internal pass are fetched up front, before the tile's loads are
-    // issued, so their latency overlaps the data's (fetched inside the pass
-    // they were issued only after the loads landed: ncu showed the warps
-    // waiting on one scoreboard for both)
-    // (measured slower on N = 2^28: 76 registers, 3 CTAs per SM; opt-in)
-#ifdef SFFT_PASS_PRE0
-    constexpr bool PRE0 = FactorTw<T>::value && !S0 && !PRE;
+    // fp32 groups after the first: the factor of stage S+s at index
+    // q = c + (x << S), x < 2^(s-1), is w_{S+s}(c) * w_s(x).  The CTA looks
+    // the column parts w_{S+s}(c) up once per tile ([L][TJ] in shared memory,
+    // L*TJ two-level lookups instead of L/LR*R per thread) while the tile's
+    // loads are in flight; the x part is a small-stage table entry.
+#ifdef SFFT_PASS_NO_CSTAGE
+    constexpr bool CST = false;
 #else
-    constexpr bool PRE0 = false;
+    constexpr bool CST = FactorTw<T>::value && !S0 && !PRE;
 #endif
-    constexpr int PP0 = DIF ? NPI - 1 : 0;   // the first internal pass
-    vec2_t<T> pre0[R];
-    if constexpr (PRE0) {
-        const int sp = PP0 * LR;
-        const int kp = cmin(LR, L - sp);
-        const int nsp = 1 << sp;
-#pragma unroll
-        for (int u = 0; u < R / (1 << kp); ++u) {
-            const int jp = t + P * u;
-            const I cb = (I)(c + ((uint32_t)(jp & (nsp - 1)) << S));
-#pragma unroll
-            for (int tt = 1; tt <= kp; ++tt) pre0[u * kp + tt - 1] = tw.get(S + sp + tt, cb);
+    auto stage_columns = [&]() {
+        if constexpr (CST) {
+            for (int k = tid; k < L * TJ; k += NT) {
+                const int st = k / TJ, l = k - st * TJ;
+                cs[k] = tw.get(S + 1 + st, (I)((j0 + (uint32_t)l) & (ns - 1u)));
+            }
+            __syncthreads();
         }
-    }
+    };
+    // base factors of stages S+sp+1 .. S+sp+KP for internal thread jp
+    auto column_factors = [&](int sp, int KP, int jp, vec2_t<T> *cf) {
+        const int x = jp & ((1 << sp) - 1);
+        for (int tt = 1; tt <= KP; ++tt) {
+            vec2_t<T> w = cs[(sp + tt - 1) * TJ + jl];
+            if (sp > 0) {
+                const vec2_t<T> sm = ldtw(tw.tab + ((1 << (sp + tt - 1)) - 1) + x);
+                T r, i;
+                cmul(w.x, w.y, sm.x, sm.y, r, i);
+                w.x = r;
+                w.y = i;
+            }
+            cf[tt - 1] = w;
+        }
+    };
+
     if constexpr (PRE) {
 #pragma unroll
         for (int pp = 0; pp < NPI; ++pp) {
@@ -383,12 +405,15 @@ sfft_pass_kernel(const PassArgs a)
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \
+        if (pp == 0) stage_columns();                                                           \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                           \
         {                                                                                       \
             const int jp = t + P * u;                                                           \
+            vec2_t<T> cf[KP];                                                                   \
+            if constexpr (CST) column_factors(sp, KP, jp, cf);                                  \
             dit_stages<T, KP, S0>(v + u * RP, S + sp,                             \
                                   (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw,               \
-                                  PRE ? &pre[pp][u * KP] : (PRE0 && pp == PP0) ? &pre0[u * KP] : nullptr);                            \
+                                  CST ? cf : PRE ? &pre[pp][u * KP] : nullptr);                 \
         }                                                                                       \
         if (DIST && pp == 0) discard_tile();                                                    \
         const bool last = pp == NPI - 1;                                                        \
@@ -473,12 +498,15 @@ sfft_pass_kernel(const PassArgs a)
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \
+        if (first) stage_columns();                                                             \
         _Pragma("unroll") for (int u = 0; u < U; ++u)                                           \
         {                                                                                       \
             const int jp = t + P * u;                                                           \
+            vec2_t<T> cf[KP];                                                                   \
+            if constexpr (CST) column_factors(sp, KP, jp, cf);                                  \
             dif_stages<T, KP, S0>(v + u * RP, S + sp,                             \
                                   (I)(c + ((uint32_t)(jp & (nsp - 1)) << S)), tw,               \
-                                  PRE ? &pre[pp][u * KP] : (PRE0 && pp == PP0) ? &pre0[u * KP] : nullptr);                            \
+                                  CST ? cf : PRE ? &pre[pp][u * KP] : nullptr);                 \
         }                                                                                       \
         if (pp != 0) {                                                                          \
             if (!first || S0) __syncthreads();                                                  \
