@@ -455,8 +455,9 @@ sfft_pass_kernel(const PassArgs a)
             // outputs of this tile are the contiguous rows j0..j0+TJ of 2^L:
             // copy smem [o][jl] -> global in linear order
             const uint32_t obase = j0 * SUB;
-            for (int k = tid; k < TJ * SUB; k += NT) {
-                const int jj = k >> L, o = k & (SUB - 1);
+#pragma unroll
+            for (int kk = 0; kk < R; ++kk) {
+                const int k = tid + kk * NT, jj = k >> L, o = k & (SUB - 1);
                 put_out(oaddr(obase + k), sr[o * RS + jj], si[o * RS + jj]);
             }
         }
@@ -464,13 +465,18 @@ sfft_pass_kernel(const PassArgs a)
         // ------------------------------ DIF ------------------------------
         if constexpr (S0) {
             // inputs are the contiguous rows j0..j0+TJ of 2^L: stage them
+            // (all R loads of a thread first, then the shared stores: the
+            // loop written load->store serialised the load latencies, 2x
+            // slower than the DIT S = 0 launch)
             const uint32_t ibase = j0 * SUB;
-            for (int k = tid; k < TJ * SUB; k += NT) {
-                const int jj = k >> L, o = k & (SUB - 1);
-                T re, im;
-                get_in(iaddr(ibase + k), re, im);
-                sr[o * RS + jj] = re;
-                si[o * RS + jj] = im;
+            static_assert(TJ * SUB == R * NT, "one tile = R elements per thread");
+#pragma unroll
+            for (int kk = 0; kk < R; ++kk) get_in(iaddr(ibase + tid + kk * NT), v[kk].x, v[kk].y);
+#pragma unroll
+            for (int kk = 0; kk < R; ++kk) {
+                const int k = tid + kk * NT, jj = k >> L, o = k & (SUB - 1);
+                sr[o * RS + jj] = v[kk].x;
+                si[o * RS + jj] = v[kk].y;
             }
             __syncthreads();
         }
