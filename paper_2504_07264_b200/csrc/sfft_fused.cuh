@@ -42,15 +42,15 @@ struct GIO<T, false> {
     int64_t is, os;
     bool inv;
     T scale;
+    // the inverse's input channel swap is a plane-pointer exchange (no
+    // per-element selects); its output swap + 1/N stays a uniform branch
     __device__ __forceinline__ GIO(const FusedArgs &a)
-        : xr((const T *)a.x0), xi((const T *)a.x1), yr((T *)a.y0), yi((T *)a.y1),
-          is(a.in_stride), os(a.out_stride), inv(a.inverse != 0), scale((T)a.scale) {}
+        : xr((const T *)(a.inverse ? a.x1 : a.x0)), xi((const T *)(a.inverse ? a.x0 : a.x1)), yr((T *)a.y0),
+          yi((T *)a.y1), is(a.in_stride), os(a.out_stride), inv(a.inverse != 0), scale((T)a.scale) {}
     __device__ __forceinline__ void load(int64_t row, int64_t e, T &re, T &im) const
     {
-        const T a = ld_stream(xr + row * is + e);
-        const T b = ld_stream(xi + row * is + e);
-        re = inv ? b : a;
-        im = inv ? a : b;
+        re = ld_stream(xr + row * is + e);
+        im = ld_stream(xi + row * is + e);
     }
     __device__ __forceinline__ void store(int64_t row, int64_t e, T re, T im) const
     {
