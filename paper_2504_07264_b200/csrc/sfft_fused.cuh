@@ -32,11 +32,16 @@ struct FusedArgs {
 };
 
 // Global-memory view of the caller's rows.
-template <typename T, bool IL>
+// RB: the row is folded into the pointers once (rebase) and per-element
+// addresses are base + constant.  Used by DIF, whose first-pass index
+// expression made the compiler recompute row * stride + e per element (~7
+// instructions per access; N = 4096 DIF 0.78 -> 0.88 of peak); DIT measured
+// 4% slower with it and keeps the row term.
+template <typename T, bool IL, bool RB = false>
 struct GIO;
 
-template <typename T>
-struct GIO<T, false> {
+template <typename T, bool RB>
+struct GIO<T, false, RB> {
     const T *xr, *xi;
     T *yr, *yi;
     int64_t is, os;
@@ -47,25 +52,34 @@ struct GIO<T, false> {
     __device__ __forceinline__ GIO(const FusedArgs &a)
         : xr((const T *)(a.inverse ? a.x1 : a.x0)), xi((const T *)(a.inverse ? a.x0 : a.x1)), yr((T *)a.y0),
           yi((T *)a.y1), is(a.in_stride), os(a.out_stride), inv(a.inverse != 0), scale((T)a.scale) {}
+    __device__ __forceinline__ void rebase(int64_t row)
+    {
+        xr += row * is;
+        xi += row * is;
+        yr += row * os;
+        yi += row * os;
+    }
     __device__ __forceinline__ void load(int64_t row, int64_t e, T &re, T &im) const
     {
-        re = ld_stream(xr + row * is + e);
-        im = ld_stream(xi + row * is + e);
+        const int64_t o = RB ? e : row * is + e;
+        re = ld_stream(xr + o);
+        im = ld_stream(xi + o);
     }
     __device__ __forceinline__ void store(int64_t row, int64_t e, T re, T im) const
     {
+        const int64_t o = RB ? e : row * os + e;
         if (inv) {
-            st_stream(yr + row * os + e, im * scale);
-            st_stream(yi + row * os + e, re * scale);
+            st_stream(yr + o, im * scale);
+            st_stream(yi + o, re * scale);
         } else {
-            st_stream(yr + row * os + e, re);
-            st_stream(yi + row * os + e, im);
+            st_stream(yr + o, re);
+            st_stream(yi + o, im);
         }
     }
 };
 
-template <typename T>
-struct GIO<T, true> {
+template <typename T, bool RB>
+struct GIO<T, true, RB> {
     using V = vec2_t<T>;
     const V *x;
     V *y;
@@ -75,9 +89,14 @@ struct GIO<T, true> {
     __device__ __forceinline__ GIO(const FusedArgs &a)
         : x((const V *)a.x0), y((V *)a.y0), is(a.in_stride), os(a.out_stride),
           inv(a.inverse != 0), scale((T)a.scale) {}
+    __device__ __forceinline__ void rebase(int64_t row)
+    {
+        x += row * is;
+        y += row * os;
+    }
     __device__ __forceinline__ void load(int64_t row, int64_t e, T &re, T &im) const
     {
-        const V v = ld_stream(x + row * is + e);
+        const V v = ld_stream(x + (RB ? e : row * is + e));
         re = inv ? v.y : v.x;
         im = inv ? v.x : v.y;
     }
@@ -91,7 +110,7 @@ struct GIO<T, true> {
             v.x = re;
             v.y = im;
         }
-        st_stream(y + row * os + e, v);
+        st_stream(y + (RB ? e : row * os + e), v);
     }
 };
 
@@ -123,7 +142,7 @@ __device__ __forceinline__ void sig_sync()
 // ---- DIT pass p -----------------------------------------------------------
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL> &io,
+                                         T *sr, T *si, const GIO<T, IL, false> &io,
                                          const TwCat<T> &tw, const vec2_t<T> *pre)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
@@ -186,7 +205,7 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dit_from(vec2_t<T> *v, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw,
+                                         T *sr, T *si, const GIO<T, IL, false> &io, const TwCat<T> &tw,
                                          const vec2_t<T> *pre)
 {
     if constexpr (p < FusedShape<LOGN, LR_REQ>::NPASS) {
@@ -198,7 +217,7 @@ __device__ __forceinline__ void dit_from(vec2_t<T> *v, int t, int64_t row, bool 
 // ---- DIF pass p (executed for p = NPASS-1 .. 0) --------------------------
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL> &io,
+                                         T *sr, T *si, const GIO<T, IL, true> &io,
                                          const TwCat<T> &tw, const vec2_t<T> *pre)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
@@ -259,7 +278,7 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dif_from(vec2_t<T> *v, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL> &io, const TwCat<T> &tw,
+                                         T *sr, T *si, const GIO<T, IL, true> &io, const TwCat<T> &tw,
                                          const vec2_t<T> *pre)
 {
     if constexpr (p >= 0) {
@@ -288,7 +307,8 @@ sfft_fused_kernel(const FusedArgs a)
     const int sl = tid / P, t = tid % P;
     const int64_t row = (int64_t)blockIdx.x * S + sl;
     const bool valid = row < a.batch;
-    const GIO<T, IL> io(a);
+    GIO<T, IL, DIF> io(a);
+    if constexpr (DIF) io.rebase(row);
     const TwCat<T> tw{reinterpret_cast<const vec2_t<T> *>(a.tw)};
 
     if constexpr (LOGN == 0) {

@@ -19,11 +19,14 @@ if [ -d "$GRAFT_REPO_ROOT/ab_old/csrc" ] && [ -n "$WITH_OLD" ]; then
   make -C $d/paper_2504_07264_b200/csrc -B -j16 > $d.log 2>&1 || { tail -5 $d.log; exit 1; }
   DIRS+=("old:$d")
 fi
+# ALGOS: "dit" (default) and/or "dif"
 for C in ${CONFIGS:-cfg2_n64_f32}; do
-  for i in 1 2; do
+ for A in ${ALGOS:-dit}; do
+  for i in $(seq ${REPS:-2}); do
     for nd in "${DIRS[@]}"; do
       n=${nd%%:*}; d=${nd#*:}
-      (cd $d && python bench.py --config $C --steps 100 --warmup 10 --no-cpu-baseline --no-e2e | python -c "import json,sys;d=json.loads(sys.stdin.read());print('$n', '$C', round(d['ms_per_step'],5), round(d['roofline']['frac'],4), d['clocks'].get('sm_mhz'), d['clocks'].get('reasons'))")
+      (cd $d && python bench.py --config $C --algorithm $A --steps 100 --warmup 10 --no-cpu-baseline --no-e2e | python -c "import json,sys;d=json.loads(sys.stdin.read());print('$n', '$C', '$A', round(d['ms_per_step'],5), round(d['roofline']['frac'],4), d['clocks'].get('sm_mhz'), d['clocks'].get('reasons'))")
     done
   done
+ done
 done
