@@ -120,10 +120,19 @@ struct FusedShape {
     static constexpr int LR = LOGN == 0 ? 0 : cmin(LR_REQ, LOGN);
     static constexpr int R = 1 << LR;
     static constexpr int P = N / R;                       // threads per signal
-    static constexpr int NT = P > 256 ? P : 256;          // threads per block
+    // threads per block: one signal's P threads, at least 256 (128 for radix
+    // 32: 64 register values per thread; gen_inst.py fused_nt mirrors this)
+    static constexpr int NTMIN = LR >= 5 ? 128 : 256;
+    static constexpr int NT = P > NTMIN ? P : NTMIN;
     static constexpr int S = NT / P;                      // signals per block
 #ifdef SFFT_FUSED_MINB
     static constexpr int MINB = SFFT_FUSED_MINB * NT > 2048 ? 2048 / NT : SFFT_FUSED_MINB;
+#else
+    // radix 32 only (sfft_fused_kernel_r32): <= 168 registers so three
+    // 128-thread CTAs fit an SM (the compiler's own choice, 170, rounds to 176
+    // and leaves two).  Other shapes carry no min-blocks hint: an explicit 1
+    // is not the default (fp64 N = 1024 radix 8: 64 -> 116 registers).
+    static constexpr int MINB = 3;
 #endif
     static constexpr int NPASS = LOGN == 0 ? 0 : (LOGN + LR - 1) / LR;
     template <typename T>
@@ -290,13 +299,8 @@ __device__ __forceinline__ void dif_from(vec2_t<T> *v, int t, int64_t row, bool 
 // PRE (fp32 only): fetch the base factors of passes >= 1 before the data.
 // Whether that pays depends on the size (register pressure vs latency);
 // tools/tune.py measures both and gen_inst.py's AUTO table records the pick.
-template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL, bool PRE = false>
-#ifdef SFFT_FUSED_MINB
-__global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT, FusedShape<LOGN, LR_REQ>::MINB)
-#else
-__global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT)
-#endif
-sfft_fused_kernel(const FusedArgs a)
+template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL, bool PRE>
+__device__ __forceinline__ void fused_body(const FusedArgs &a)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
     constexpr int R = Sh::R, P = Sh::P, S = Sh::S, SSTR = Sh::template sstr<T>();
@@ -344,6 +348,37 @@ sfft_fused_kernel(const FusedArgs a)
             dit_from<T, LOGN, LR_REQ, IL, 0>(v, t, row, valid, sr, si, io, tw,
                                              (PRE && FactorTw<T>::value) ? pre : nullptr);
     }
+}
+
+#ifdef SFFT_FUSED_MINB
+template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL, bool PRE = false>
+__global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT, FusedShape<LOGN, LR_REQ>::MINB)
+sfft_fused_kernel(const FusedArgs a)
+{
+    fused_body<T, LOGN, LR_REQ, DIF, IL, PRE>(a);
+}
+#else
+template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL, bool PRE = false>
+__global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT)
+sfft_fused_kernel(const FusedArgs a)
+{
+    fused_body<T, LOGN, LR_REQ, DIF, IL, PRE>(a);
+}
+#endif
+
+template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL, bool PRE = false>
+__global__ void __launch_bounds__(FusedShape<LOGN, LR_REQ>::NT, FusedShape<LOGN, LR_REQ>::MINB)
+sfft_fused_kernel_r32(const FusedArgs a)
+{
+    fused_body<T, LOGN, LR_REQ, DIF, IL, PRE>(a);
+}
+
+// the kernel a shape launches: radix 32 takes the register-capped variant
+template <typename T, int LOGN, int LR_REQ, bool DIF, bool IL, bool PRE>
+constexpr auto fused_kernel_for()
+{
+    if constexpr (FusedShape<LOGN, LR_REQ>::LR >= 5) return &sfft_fused_kernel_r32<T, LOGN, LR_REQ, DIF, IL, PRE>;
+    else return &sfft_fused_kernel<T, LOGN, LR_REQ, DIF, IL, PRE>;
 }
 
 }  // namespace sfft

@@ -82,8 +82,6 @@ def test_f32_rel_l2_vs_oracle(cuda, m, algo, inverse):
 @pytest.mark.parametrize("m,lr", [(m, lr) for m in (4, 5, 6, 7, 9, 10, 11, 12) for lr in (2, 3, 4, 5)
                                   if (1 << (m - min(lr, m))) <= 1024])
 def test_every_radix_schedule(cuda, m, lr, algo, dtype, prefetch):
-    if dtype == np.float64 and lr == 5:
-        pytest.skip("fp64 register radix is capped at 2^4")
     if dtype == np.float64 and prefetch:
         pytest.skip("fp64 reads every factor from the table")
     rng = np.random.default_rng(3000 + 16 * m + lr)

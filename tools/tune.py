@@ -56,7 +56,7 @@ def main():
             xr = torch.randn(b, n, dtype=tdt, device="cuda")
             xi = torch.randn(b, n, dtype=tdt, device="cuda")
             yr, yi = torch.empty_like(xr), torch.empty_like(xi)
-            variants = [("ldg", lr, None) for lr in range(1, 6 if dt == "f32" else 5)
+            variants = [("ldg", lr, None) for lr in range(1, 6)
                         if lr <= m and (n >> lr) <= 1024]
             variants += [("tma", lr, None) for lr in TMA_LR[dt].get(m, [])]
             if dt == "f32":   # both settings of the up-front base factors
