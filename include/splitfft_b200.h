@@ -55,6 +55,8 @@ extern "C" {
 #define SFFT_KERNEL_LDG 1   /* per-thread global loads/stores (any stride/alignment, interleaved) */
 #define SFFT_KERNEL_TMA 2   /* require the TMA kernel (planar, 16-byte aligned rows and strides) */
 #define SFFT_KERNEL_PASS 3  /* reported by sfft_plan_info for the multi-launch path (log2n > 12) */
+#define SFFT_KERNEL_PAIR 4  /* fp32 planar: two signals per thread, packed across the pair (batch >= 2;
+                               odd batches pad the last pair, other layouts take the LDG kernel) */
 
 /* plan limit, transform.py:32 (MAX_PLAN_M) */
 #define SFFT_MAX_LOG2N 30

@@ -141,6 +141,7 @@ struct sfft_plan {
     int log2n = 0, dtype = 0, algo = 0, device = 0, lr = 0;
     int kernel = SFFT_KERNEL_AUTO;  // fused-path kernel family
     int lr_tma = -1;                // radix of the TMA kernel (-1: none)
+    int lr_pair = -1;               // radix of the fp32 pair kernel (-1: none)
     int lr_ldg_il = 0;              // radix of the interleaved LDG kernel
     bool pre = false;               // fp32: fetch pass base factors up front
     // fused path
@@ -491,6 +492,25 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         const bool aligned = ((uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)y0 | (uintptr_t)y1) % 16 == 0 &&
                              ((size_t)is * esz) % 16 == 0 && ((size_t)os * esz) % 16 == 0 &&
                              batch < (int64_t(1) << 31);
+        if (!il && p->lr_pair >= 0 && batch >= 2) {
+            FusedLaunchFn pf = fused_pair_launcher(m, p->lr_pair, p->algo == SFFT_DIF);
+            if (pf) {
+                FusedArgs a;
+                a.x0 = x0;
+                a.x1 = x1;
+                a.y0 = y0;
+                a.y1 = y1;
+                a.tw = p->d_tw;
+                a.batch = batch;
+                a.in_stride = is;
+                a.out_stride = os;
+                a.inverse = inv ? 1 : 0;
+                a.scale = scale;
+                cudaError_t e = pf(a, p->algo == SFFT_DIF, false, st);
+                if (e != cudaSuccess) return cuda_fail(e, "pair kernel launch");
+                return SFFT_OK;
+            }
+        }
         if (!il && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG && aligned) {
             TmaLaunchFn tf = tma_launcher(p->dtype, m, p->lr_tma, p->algo == SFFT_DIF, p->pre);
             if (tf) {
@@ -688,7 +708,8 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
     if (dtype != SFFT_F32 && dtype != SFFT_F64) return fail(SFFT_EINVAL, "unknown dtype %d", dtype);
     const int pre_pref = (kernel >> 4) & 3;   // 0 auto, 1 off, 2 on
     kernel &= 0xf;
-    if ((kernel != SFFT_KERNEL_AUTO && kernel != SFFT_KERNEL_LDG && kernel != SFFT_KERNEL_TMA) || pre_pref == 3)
+    if ((kernel != SFFT_KERNEL_AUTO && kernel != SFFT_KERNEL_LDG && kernel != SFFT_KERNEL_TMA &&
+         kernel != SFFT_KERNEL_PAIR) || pre_pref == 3)
         return fail(SFFT_EINVAL, "unknown kernel family %d", kernel);
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -708,9 +729,14 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
     int rc = SFFT_OK;
     p->kernel = kernel;
     if (log2n <= kFusedMaxLog) {
-        bool auto_tma = false, auto_pre = false;
-        int auto_lr = 0;
-        auto_choice(dtype, log2n, &auto_tma, &auto_lr, &auto_pre);
+        bool auto_pre = false;
+        int auto_lr = 0, auto_family = 0;
+        auto_choice(dtype, log2n, &auto_family, &auto_lr, &auto_pre);
+        const bool auto_tma = auto_family == 1, auto_pair = auto_family == 2;
+        if (kernel == SFFT_KERNEL_PAIR && (dtype != SFFT_F32 || log2n < 1)) {
+            delete p;
+            return fail(SFFT_EINVAL, "the pair kernel is fp32 only (log2n >= 1)");
+        }
         p->pre = pre_pref == 2 || (pre_pref == 0 && kernel == SFFT_KERNEL_AUTO && log2_radix <= 0 && auto_pre);
         int lr;
         if (log2_radix > 0) lr = log2_radix;
@@ -728,6 +754,13 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
         const bool want_tma = kernel == SFFT_KERNEL_TMA ||
                               (kernel == SFFT_KERNEL_AUTO && (log2_radix > 0 || auto_tma));
         if (want_tma && tma_launcher(dtype, log2n, lr, false, p->pre)) p->lr_tma = lr;
+        const bool want_pair = kernel == SFFT_KERNEL_PAIR ||
+                               (kernel == SFFT_KERNEL_AUTO && log2_radix <= 0 && auto_pair);
+        if (want_pair && fused_pair_launcher(log2n, lr, false)) p->lr_pair = lr;
+        if (kernel == SFFT_KERNEL_PAIR && p->lr_pair < 0) {
+            delete p;
+            return fail(SFFT_EINVAL, "no pair kernel for log2n=%d radix=2^%d", log2n, lr);
+        }
         if (kernel == SFFT_KERNEL_TMA && p->lr_tma < 0) {
             delete p;
             return fail(SFFT_EINVAL, "no TMA kernel for log2n=%d radix=2^%d", log2n, lr);
@@ -769,7 +802,10 @@ int sfft_plan_destroy(sfft_plan *plan)
 int sfft_plan_info(const sfft_plan *p, int *log2n, int *dtype, int *algorithm, int *device, int *launches,
                    int *log2_radix, int *kernel)
 {
-    if (kernel && p) *kernel = p->lr_tma >= 0 ? SFFT_KERNEL_TMA : (p->log2n <= kFusedMaxLog ? SFFT_KERNEL_LDG : SFFT_KERNEL_PASS);
+    if (kernel && p)
+        *kernel = p->lr_pair >= 0  ? SFFT_KERNEL_PAIR
+                  : p->lr_tma >= 0 ? SFFT_KERNEL_TMA
+                                   : (p->log2n <= kFusedMaxLog ? SFFT_KERNEL_LDG : SFFT_KERNEL_PASS);
     if (!p) return fail(SFFT_EINVAL, "plan is NULL");
     if (log2n) *log2n = p->log2n;
     if (dtype) *dtype = p->dtype;

@@ -47,7 +47,11 @@ TmaLaunchFn tma_launcher(int dtype, int logn, int lr, bool dif, bool pre = false
 TmaLaunchFn tma_launcher_f32(int logn, int lr, bool dif, bool pre);
 TmaLaunchFn tma_launcher_f64(int logn, int lr, bool dif, bool pre);
 int tma_default_lr(int dtype, int logn);   // -1: no TMA config for this size
-void auto_choice(int dtype, int logn, bool *tma, int *lr, bool *pre);  // kernel=auto pick, 0 <= logn <= 12
+// kernel=auto pick, 0 <= logn <= 12: family 0 = LDG fused, 1 = TMA, 2 = pair (fp32)
+void auto_choice(int dtype, int logn, int *family, int *lr, bool *pre);
+// fp32 planar fused kernel with two signals per thread (sfft_fused_pair.cuh);
+// bound to dif, ignores the (dif, il) arguments
+FusedLaunchFn fused_pair_launcher(int logn, int lr, bool dif);
 
 PassTmaLaunchFn pass_tma_launcher(int dtype, int L, bool dif);
 PassTmaLaunchFn pass_tma_launcher_f32(int L, bool dif);

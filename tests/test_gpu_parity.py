@@ -94,6 +94,45 @@ def test_every_radix_schedule(cuda, m, lr, algo, dtype, prefetch):
         assert rel_l2(gr.astype(np.float64), gi.astype(np.float64), wr, wi) <= F32_TOL(m)
 
 
+@pytest.mark.parametrize("inverse", [False, True])
+@pytest.mark.parametrize("algo", ["dit", "dif"])
+@pytest.mark.parametrize("m,lr,b", [(m, lr, b) for m in (4, 6, 8, 10, 11, 12) for lr in (2, 3, 4)
+                                    if (1 << (m - min(lr, m))) <= 1024 for b in (2, 7)])
+def test_pair_kernel(cuda, m, lr, b, algo, inverse):
+    """fp32 two-signals-per-thread kernel: the single-signal kernel's values
+    (same per-lane rounding) and the oracle tolerance; odd batches pad the
+    last pair."""
+    rng = np.random.default_rng(5000 + 16 * m + lr + b)
+    re, im = rand(rng, b, 1 << m, np.float32)
+    plan = sf.make_plan(m, algo, dtype=torch.float32, device="cuda:0", radix_log=lr, kernel="pair")
+    assert plan.kernel == "pair"
+    yr, yi = sf.fft_split(torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda(), inverse=inverse, plan=plan)
+    gr, gi = yr.cpu().numpy(), yi.cpu().numpy()
+    ldg = sf.make_plan(m, algo, dtype=torch.float32, device="cuda:0", radix_log=lr, kernel="ldg",
+                       prefetch_factors=False)
+    lr_, li_ = sf.fft_split(torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda(), inverse=inverse, plan=ldg)
+    assert np.array_equal(gr.view(np.int32), lr_.cpu().numpy().view(np.int32))
+    assert np.array_equal(gi.view(np.int32), li_.cpu().numpy().view(np.int32))
+    wr, wi = oracle.fft_split_c(re, im, algo, inverse)
+    assert rel_l2(gr.astype(np.float64), gi.astype(np.float64), wr, wi) <= F32_TOL(m)
+
+
+@pytest.mark.parametrize("stride_pad", [0, 5])
+def test_pair_kernel_strides_and_single_row(cuda, stride_pad):
+    """Row strides other than N, and batch 1 (which takes the LDG kernel)."""
+    m = 10
+    n = 1 << m
+    rng = np.random.default_rng(77 + stride_pad)
+    big_r = torch.from_numpy(rng.standard_normal((5, n + stride_pad)).astype(np.float32)).cuda()
+    big_i = torch.from_numpy(rng.standard_normal((5, n + stride_pad)).astype(np.float32)).cuda()
+    xr, xi = big_r[:, :n], big_i[:, :n]
+    plan = sf.make_plan(m, "dit", dtype=torch.float32, device="cuda:0", radix_log=4, kernel="pair")
+    for rows in (5, 1):
+        yr, yi = sf.fft_split(xr[:rows], xi[:rows], plan=plan)
+        wr, wi = oracle.fft_split_c(xr[:rows].cpu().numpy(), xi[:rows].cpu().numpy(), "dit", False)
+        assert rel_l2(yr.cpu().numpy().astype(np.float64), yi.cpu().numpy().astype(np.float64), wr, wi) <= F32_TOL(m)
+
+
 @pytest.mark.parametrize("m", [3, 6, 10, 12, 14])
 @pytest.mark.parametrize("algo", ["dit", "dif"])
 def test_interleaved_in_place_matches_split(cuda, m, algo):
