@@ -21,6 +21,8 @@
 
 namespace sfft {
 
+template <int V> struct IntC { static constexpr int value = V; };
+
 struct FusedArgs {
     const void *x0, *x1;   // planar: re, im planes; interleaved: x0 = pairs
     void *y0, *y1;
@@ -148,6 +150,37 @@ __device__ __forceinline__ void sig_sync()
     if constexpr (P <= 32) __syncwarp(); else __syncthreads();
 }
 
+// Partial last exchange.  When the last register pass runs KPL < LR stages
+// (RPL = 2^KPL), the exchange before it only permutes values inside groups
+// of RPL threads: thread t of group position g = t / (P/RPL) needs, for
+// each u < R/RPL, the value of Stockham position f = g + RPL*u from each
+// group member -- and the one from itself it already holds.  So each thread
+// keeps 1/RPL of its values in registers and moves only the rest through
+// shared memory (fp64 N = 1024, radix 8, passes 3+3+3+1: the last exchange
+// shrinks by half).  g is warp-uniform when P/RPL >= 32; the code is
+// specialised per g (compile-time register indices).
+template <int LOGN, int LR_REQ>
+struct LastX {
+    using Sh = FusedShape<LOGN, LR_REQ>;
+    static constexpr int KPL = Sh::NPASS >= 1 ? LOGN - (Sh::NPASS - 1) * Sh::LR : 0;
+    static constexpr int RPL = 1 << KPL;
+#ifdef SFFT_NO_PARTIAL_EXCHANGE
+    static constexpr bool on = false;
+#else
+    static constexpr bool on = Sh::NPASS >= 2 && KPL < Sh::LR && Sh::P / RPL >= 32;
+#endif
+    static constexpr int GSTRIDE = Sh::P / RPL;      // threads per group position
+};
+
+template <int G, int N_, typename F>
+__device__ __forceinline__ void with_g(int g, F &&f)
+{
+    if constexpr (G < N_) {
+        if (g == G) f(IntC<G>{});
+        else with_g<G + 1, N_>(g, f);
+    }
+}
+
 // ---- DIT pass p -----------------------------------------------------------
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool valid,
@@ -161,7 +194,32 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
     constexpr int RP = 1 << KP, U = R / RP, NS = 1 << SP;
     constexpr bool FIRST = p == 0, LAST = p == Sh::NPASS - 1;
 
+    using LX = LastX<LOGN, LR_REQ>;
     // gather this pass's inputs
+    if constexpr (LAST && !FIRST && LX::on) {
+        // own values: Stockham position f = G + RP*u of the previous pass,
+        // held in register brev(f, LR) (copied out before v is overwritten)
+        with_g<0, RP>(t / LX::GSTRIDE, [&](auto GC) {
+            constexpr int G = decltype(GC)::value;
+            vec2_t<T> own[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) own[u] = v[brev(G + RP * u, LR)];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = t + P * u;
+#pragma unroll
+                for (int r = 0; r < RP; ++r) {
+                    const int e = j + r * (N / RP);
+                    if (r == G) {
+                        v[u * RP + r] = own[u];
+                    } else {
+                        v[u * RP + r].x = sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
+                        v[u * RP + r].y = si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
+                    }
+                }
+            }
+        });
+    } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = t + P * u;
@@ -177,6 +235,7 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
             }
         }
     }
+    }
     // stages SP+1 .. SP+KP
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -187,6 +246,21 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
     // scatter in Stockham order
     if constexpr (!LAST) {
         if constexpr (!FIRST) sig_sync<P>();
+        if constexpr (p == Sh::NPASS - 2 && LX::on) {
+            // partial last exchange: positions f = G (mod RPL) stay in registers
+            static_assert(U == 1, "the pass before the last runs the full radix");
+            with_g<0, LX::RPL>(t / LX::GSTRIDE, [&](auto GC) {
+                constexpr int G = decltype(GC)::value;
+                const int base = (t >> SP) * NS * RP + (t & (NS - 1));
+#pragma unroll
+                for (int f = 0; f < RP; ++f) {
+                    if (f % LX::RPL == G) continue;
+                    const int e = base + NS * f;
+                    sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[brev(f, KP)].x;
+                    si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[brev(f, KP)].y;
+                }
+            });
+        } else {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int j = t + P * u;
@@ -197,6 +271,7 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].x;
                 si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].y;
             }
+        }
         }
         sig_sync<P>();
     } else {
@@ -235,7 +310,32 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
     constexpr int KP = cmin(LR, LOGN - SP);
     constexpr int RP = 1 << KP, U = R / RP, NS = 1 << SP;
     constexpr bool FIRST = p == Sh::NPASS - 1, LAST = p == 0;
+    using LX = LastX<LOGN, LR_REQ>;
 
+    if constexpr (p == Sh::NPASS - 2 && LX::on) {
+        // partial exchange (transpose of the DIT one): position f = G + RPL*u'
+        // is this thread's own register u'*RPL + G of the previous pass
+        static_assert(U == 1, "the pass after the first runs the full radix");
+        with_g<0, LX::RPL>(t / LX::GSTRIDE, [&](auto GC) {
+            constexpr int G = decltype(GC)::value;
+            constexpr int UL = R / LX::RPL;
+            vec2_t<T> own[UL];
+#pragma unroll
+            for (int u = 0; u < UL; ++u) own[u] = v[u * LX::RPL + G];
+            const int base = (t >> SP) * NS * RP + (t & (NS - 1));
+#pragma unroll
+            for (int f = 0; f < RP; ++f) {
+                const int e = base + NS * f;
+                const int d = brev(f, KP);
+                if (f % LX::RPL == G) {
+                    v[d] = own[f / LX::RPL];
+                } else {
+                    v[d].x = sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
+                    v[d].y = si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
+                }
+            }
+        });
+    } else {
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = t + P * u;
@@ -253,6 +353,7 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
             }
         }
     }
+    }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const int j = t + P * u;
@@ -261,6 +362,23 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
     }
     if constexpr (!LAST) {
         if constexpr (!FIRST) sig_sync<P>();
+        if constexpr (FIRST && LX::on) {
+            // partial exchange: r == G stays in registers for the next pass
+            with_g<0, RP>(t / LX::GSTRIDE, [&](auto GC) {
+                constexpr int G = decltype(GC)::value;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = t + P * u;
+#pragma unroll
+                    for (int r = 0; r < RP; ++r) {
+                        if (r == G) continue;
+                        const int e = j + r * (N / RP);
+                        sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].x;
+                        si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].y;
+                    }
+                }
+            });
+        } else {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int j = t + P * u;
@@ -270,6 +388,7 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].x;
                 si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].y;
             }
+        }
         }
         sig_sync<P>();
     } else {

@@ -106,3 +106,40 @@ def test_register_pass_map_is_bitwise_the_reference(m, logr):
     for algo, model in (("dit", model_dit), ("dif", model_dif)):
         wr, wi = oracle.fft_split_c(x.real.copy(), x.imag.copy(), algo)
         assert np.array_equal(bits(model(x, m, logr)), bits(wr + 1j * wi)), (algo, m, logr)
+
+
+@pytest.mark.parametrize("m,logr", [(m, lr) for m in range(2, 13) for lr in (2, 3, 4, 5) if lr < m])
+def test_partial_last_exchange_keeps_own_values(m, logr):
+    """sfft_fused.cuh LastX: before a last register pass of KPL < LR stages,
+    the Stockham exchange permutes values only inside groups of RPL = 2^KPL
+    threads (t = g * P/RPL + c), and the value thread t reads at (u, r = g)
+    is the one it wrote itself at position f = g + RPL*u -- so the kernels
+    keep those in registers (DIT: the gather of the last pass; DIF: the
+    transpose, first pass -> second).  Checked on the kernels' index formulas
+    for every physical thread."""
+    n, r_ = 1 << m, 1 << logr
+    p_ = n // r_
+    sched = schedule(m, logr)
+    if len(sched) < 2 or sched[-1][1] == logr:
+        return
+    sp_prev, _ = sched[-2]
+    sp_last, kpl = sched[-1]
+    rpl, ns_prev, ns_last = 1 << kpl, 1 << sp_prev, 1 << sp_last
+    gstride = p_ // rpl
+    writer = {}
+    for i in range(p_):                       # pass NPASS-2 scatter (U = 1, full radix)
+        base = (i >> sp_prev) * ns_prev * r_ + (i & (ns_prev - 1))
+        for f in range(r_):
+            writer[base + ns_prev * f] = (i, f)
+    assert len(writer) == n
+    for t in range(p_):                       # last pass gather
+        g = t // gstride
+        for u in range(r_ // rpl):
+            j = t + p_ * u
+            for r in range(rpl):
+                wi, wf = writer[j + r * (n // rpl)]
+                assert wi % gstride == t % gstride   # same group of RPL threads
+                if r == g:
+                    assert (wi, wf) == (t, g + rpl * u)
+                else:
+                    assert wi != t
