@@ -24,6 +24,8 @@
 // (m <= 30); the owner-field address maps of a sharded transform
 // (sfft_dist_*) are compiled in only for DIST launches.
 #pragma once
+#include <type_traits>
+
 #include "sfft_common.cuh"
 
 namespace sfft {
@@ -82,6 +84,16 @@ struct PassArgs {
     // that is dead)
     int keep_out, discard_in;
 };
+
+// p + k * stride_bytes as one 32x32->64 multiply-add (IMAD.WIDE.U32): the
+// strided plane addresses of a pass launch are a per-thread base plus a
+// compile-time multiple of a launch-uniform stride.
+template <typename P>
+__device__ __forceinline__ P *at_stride(P *p, uint32_t stride_bytes, uint32_t k)
+{
+    using C = typename std::conditional<std::is_const<P>::value, const char, char>::type;
+    return reinterpret_cast<P *>(reinterpret_cast<C *>(p) + (uint64_t)stride_bytes * k);
+}
 
 __device__ __forceinline__ void l2_discard(const void *p)
 {
@@ -161,6 +173,15 @@ __device__ __forceinline__ PIO<T, IL> make_pio(const PassArgs &a)
     }
     return p;
 }
+
+template <typename T>
+__device__ __forceinline__ const T *src_plane(const PIO<T, false> &p, int k) { return k ? p.ai : p.ar; }
+template <typename T>
+__device__ __forceinline__ const T *src_plane(const PIO<T, true> &, int) { return nullptr; }
+template <typename T>
+__device__ __forceinline__ T *dst_plane(const PIO<T, false> &p, int k) { return k ? p.bi : p.br; }
+template <typename T>
+__device__ __forceinline__ T *dst_plane(const PIO<T, true> &, int) { return nullptr; }
 
 // Twiddle source of a group: the S = 0 group only touches stages <= 8, all in
 // the stage-major table; later groups may need the large-stage sources.
@@ -299,6 +320,40 @@ sfft_pass_kernel(const PassArgs a)
             im = y;
         }
     };
+    // Planar, unsharded launches: per-thread plane pointers + uniform byte
+    // strides, so each strided access costs one IMAD.WIDE instead of the
+    // 32-bit index -> 64-bit offset -> scaled address sequence (~6 integer
+    // instructions per access on the S > 0 launches).
+    constexpr bool FAST_IN = !DIST && !IL_IN, FAST_OUT = !DIST && !IL_OUT;
+    const uint32_t nj_bytes = NJ * (uint32_t)sizeof(T), ns_bytes = ns * (uint32_t)sizeof(T);
+    // DIT loads / DIF stores: element j + (t + k) * NJ of the row
+    const T *in_r = nullptr, *in_i = nullptr;
+    T *out_r = nullptr, *out_i = nullptr;
+    if constexpr (FAST_IN && !DIF) {
+        const int64_t b = ioff + j + (int64_t)t * NJ;
+        in_r = (const T *)src_plane(src, 0) + b;
+        in_i = (const T *)src_plane(src, 1) + b;
+    }
+    if constexpr (FAST_OUT && DIF) {
+        const int64_t b = ooff + j + (int64_t)t * NJ;
+        out_r = (T *)dst_plane(dst, 0) + b;
+        out_i = (T *)dst_plane(dst, 1) + b;
+    }
+    // DIT stores (S > 0): element gbase + ns * (t + k)
+    if constexpr (FAST_OUT && !DIF && !S0) {
+        const int64_t b = ooff + gbase + (int64_t)ns * t;
+        out_r = (T *)dst_plane(dst, 0) + b;
+        out_i = (T *)dst_plane(dst, 1) + b;
+    }
+    auto put_fast = [&](T *pr, T *pi, T re, T im) {
+        if (swap_out) {   // planes already exchanged
+            re *= scale;
+            im *= scale;
+        }
+        st_stream(pr, re);
+        st_stream(pi, im);
+    };
+
     // after the first internal pass consumed the tile (so every load of it
     // has landed): drop the scratch lines it came from.  A line is the TJ
     // sub-problems of one element row e (128 bytes); the first thread of each
@@ -398,7 +453,15 @@ sfft_pass_kernel(const PassArgs a)
             _Pragma("unroll") for (int r = 0; r < RP; ++r)                                      \
             {                                                                                   \
                 const int e = jp + r * (SUB / RP);                                              \
-                if (pp == 0) get_in(iaddr(j + (uint32_t)e * NJ), v[u * RP + r].x, v[u * RP + r].y); \
+                if (pp == 0) {                                                                  \
+                    if constexpr (FAST_IN) {                                                    \
+                        const uint32_t k_ = (uint32_t)(P * u + r * (SUB / RP));                 \
+                        v[u * RP + r].x = ld_stream(at_stride(in_r, nj_bytes, k_));             \
+                        v[u * RP + r].y = ld_stream(at_stride(in_i, nj_bytes, k_));             \
+                    } else {                                                                    \
+                        get_in(iaddr(j + (uint32_t)e * NJ), v[u * RP + r].x, v[u * RP + r].y);  \
+                    }                                                                           \
+                }                                                                               \
                 else {                                                                          \
                     v[u * RP + r].x = sr[e * RS + jl];                                           \
                     v[u * RP + r].y = si[e * RS + jl];                                           \
@@ -438,8 +501,14 @@ sfft_pass_kernel(const PassArgs a)
                 _Pragma("unroll") for (int f = 0; f < RP; ++f)                                  \
                 {                                                                               \
                     const uint32_t o = jp + nsp * f;                                            \
-                    put_out(oaddr(gbase + ns * o), v[u * RP + brev(f, KP)].x,                    \
-                            v[u * RP + brev(f, KP)].y);                                          \
+                    if constexpr (FAST_OUT) {                                                   \
+                        const uint32_t k_ = (uint32_t)(P * u + nsp * f);                        \
+                        put_fast(at_stride(out_r, ns_bytes, k_), at_stride(out_i, ns_bytes, k_), \
+                                 v[u * RP + brev(f, KP)].x, v[u * RP + brev(f, KP)].y);         \
+                    } else {                                                                    \
+                        put_out(oaddr(gbase + ns * o), v[u * RP + brev(f, KP)].x,                \
+                                v[u * RP + brev(f, KP)].y);                                      \
+                    }                                                                           \
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \
@@ -497,7 +566,16 @@ sfft_pass_kernel(const PassArgs a)
             {                                                                                   \
                 const int e = base + nsp * f;                                                   \
                 const int d = u * RP + brev(f, KP);                                             \
-                if (first && !S0) get_in(iaddr(gbase + ns * (uint32_t)e), v[d].x, v[d].y);        \
+                if (first && !S0) {                                                             \
+                    if constexpr (FAST_IN) {                                                    \
+                        const int64_t b_ = ioff + gbase + (int64_t)ns * (uint32_t)base;         \
+                        const uint32_t k_ = (uint32_t)(nsp * f);                                \
+                        v[d].x = ld_stream(at_stride(src_plane(src, 0) + b_, ns_bytes, k_));    \
+                        v[d].y = ld_stream(at_stride(src_plane(src, 1) + b_, ns_bytes, k_));    \
+                    } else {                                                                    \
+                        get_in(iaddr(gbase + ns * (uint32_t)e), v[d].x, v[d].y);                \
+                    }                                                                           \
+                }                                                                               \
                 else {                                                                          \
                     v[d].x = sr[e * RS + jl];                                                    \
                     v[d].y = si[e * RS + jl];                                                    \
@@ -534,7 +612,13 @@ sfft_pass_kernel(const PassArgs a)
                 _Pragma("unroll") for (int r = 0; r < RP; ++r)                                  \
                 {                                                                               \
                     const int e = jp + r * (SUB / RP);                                          \
-                    put_out(oaddr(j + (uint32_t)e * NJ), v[u * RP + r].x, v[u * RP + r].y);       \
+                    if constexpr (FAST_OUT) {                                                   \
+                        const uint32_t k_ = (uint32_t)(P * u + r * (SUB / RP));                 \
+                        put_fast(at_stride(out_r, nj_bytes, k_), at_stride(out_i, nj_bytes, k_), \
+                                 v[u * RP + r].x, v[u * RP + r].y);                             \
+                    } else {                                                                    \
+                        put_out(oaddr(j + (uint32_t)e * NJ), v[u * RP + r].x, v[u * RP + r].y);   \
+                    }                                                                           \
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \
