@@ -149,7 +149,30 @@ __device__ __forceinline__ int ex_phys(int x, int e)
     using L = ExLayout<(int)sizeof(T), LOGN, LR, NT>;
     constexpr int mask = sizeof(T) == 4 ? 31 : 15;
     const int kind = L::kind(x), a = L::arg(x);
-    return kind == 0 ? e : kind == 1 ? e + (e >> a) : (e ^ ((e >> a) & mask));
+    return kind == 0 ? e
+         : kind == 1 ? e + (e >> a)
+         : kind == 3 ? e + ((e >> (a & 255)) << (a >> 8))   // shifted pad
+                     : (e ^ ((e >> a) & mask));
+}
+
+// Exchange slots split as (per-thread part) + (compile-time part) when the
+// planner proved the layout additive on that side (ExLayout::lin bit 0 =
+// Stockham writes, bit 1 = next-pass reads): e = e(t,0,0), ec = e(0,u,k), so
+// the kernel addresses the exchange as one base register plus immediates.
+template <typename T, int LOGN, int LR, int NT>
+__device__ __forceinline__ int ex_wr(int x, int e, int et, int ec)
+{
+    using L = ExLayout<(int)sizeof(T), LOGN, LR, NT>;
+    if (L::lin(x) & 1) return ex_phys<T, LOGN, LR, NT>(x, et) + ex_phys<T, LOGN, LR, NT>(x, ec);
+    return ex_phys<T, LOGN, LR, NT>(x, e);
+}
+
+template <typename T, int LOGN, int LR, int NT>
+__device__ __forceinline__ int ex_rd(int x, int e, int et, int ec)
+{
+    using L = ExLayout<(int)sizeof(T), LOGN, LR, NT>;
+    if (L::lin(x) & 2) return ex_phys<T, LOGN, LR, NT>(x, et) + ex_phys<T, LOGN, LR, NT>(x, ec);
+    return ex_phys<T, LOGN, LR, NT>(x, e);
 }
 
 template <typename T, int LOGN, int LR, int NT>

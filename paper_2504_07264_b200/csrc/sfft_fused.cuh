@@ -192,6 +192,7 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
     constexpr int SP = p * LR;
     constexpr int KP = cmin(LR, LOGN - SP);
     constexpr int RP = 1 << KP, U = R / RP, NS = 1 << SP;
+    const int et = (t >> SP) * NS * RP + (t & (NS - 1));   // this thread's write slot at u = 0, f = 0
     constexpr bool FIRST = p == 0, LAST = p == Sh::NPASS - 1;
 
     using LX = LastX<LOGN, LR_REQ>;
@@ -213,8 +214,8 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
                     if (r == G) {
                         v[u * RP + r] = own[u];
                     } else {
-                        v[u * RP + r].x = sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
-                        v[u * RP + r].y = si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
+                        v[u * RP + r].x = sr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];
+                        v[u * RP + r].y = si[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];
                     }
                 }
             }
@@ -230,8 +231,8 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 if (valid) io.load(row, e, v[u * RP + r].x, v[u * RP + r].y);
                 else { v[u * RP + r].x = T(0); v[u * RP + r].y = T(0); }
             } else {
-                v[u * RP + r].x = sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
-                v[u * RP + r].y = si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];
+                v[u * RP + r].x = sr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];
+                v[u * RP + r].y = si[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];
             }
         }
     }
@@ -256,8 +257,8 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 for (int f = 0; f < RP; ++f) {
                     if (f % LX::RPL == G) continue;
                     const int e = base + NS * f;
-                    sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[brev(f, KP)].x;
-                    si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[brev(f, KP)].y;
+                    sr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, NS * f)] = v[brev(f, KP)].x;
+                    si[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, NS * f)] = v[brev(f, KP)].y;
                 }
             });
         } else {
@@ -268,8 +269,8 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
 #pragma unroll
             for (int f = 0; f < RP; ++f) {
                 const int e = base + NS * f;
-                sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].x;
-                si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].y;
+                sr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f)] = v[u * RP + brev(f, KP)].x;
+                si[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f)] = v[u * RP + brev(f, KP)].y;
             }
         }
         }
@@ -309,6 +310,7 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
     constexpr int SP = p * LR;
     constexpr int KP = cmin(LR, LOGN - SP);
     constexpr int RP = 1 << KP, U = R / RP, NS = 1 << SP;
+    const int et = (t >> SP) * NS * RP + (t & (NS - 1));   // this thread's write slot at u = 0, f = 0
     constexpr bool FIRST = p == Sh::NPASS - 1, LAST = p == 0;
     using LX = LastX<LOGN, LR_REQ>;
 
@@ -330,8 +332,8 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 if (f % LX::RPL == G) {
                     v[d] = own[f / LX::RPL];
                 } else {
-                    v[d].x = sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
-                    v[d].y = si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
+                    v[d].x = sr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, NS * f)];
+                    v[d].y = si[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, NS * f)];
                 }
             }
         });
@@ -348,8 +350,8 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 if (valid) io.load(row, e, v[d].x, v[d].y);
                 else { v[d].x = T(0); v[d].y = T(0); }
             } else {
-                v[d].x = sr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
-                v[d].y = si[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];
+                v[d].x = sr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f)];
+                v[d].y = si[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f)];
             }
         }
     }
@@ -373,8 +375,8 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
                     for (int r = 0; r < RP; ++r) {
                         if (r == G) continue;
                         const int e = j + r * (N / RP);
-                        sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].x;
-                        si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].y;
+                        sr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].x;
+                        si[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].y;
                     }
                 }
             });
@@ -385,8 +387,8 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
 #pragma unroll
             for (int r = 0; r < RP; ++r) {
                 const int e = j + r * (N / RP);
-                sr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].x;
-                si[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].y;
+                sr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].x;
+                si[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].y;
             }
         }
         }

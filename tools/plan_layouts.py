@@ -10,6 +10,7 @@ per exchange, a layout
     none:   phys = e
     pad A:  phys = e + (e >> A)
     xor A:  phys = e ^ ((e >> A) & (banks - 1))
+    shifted pad A, B:  phys = e + ((e >> A) << B)
 plus a per-signal stride, that makes every warp-wide access of both patterns
 bank-conflict free under the shared-memory model of B300_MICROARCH.md
 (32 four-byte banks; 64-bit accesses split into two half-warp wavefronts),
@@ -56,6 +57,9 @@ def phys_fn(kind, a, esz):
         return lambda e: e
     if kind == 1:
         return lambda e: e + (e >> a)
+    if kind == 3:   # shifted pad: arg = A | B << 8, phys = e + ((e >> A) << B)
+        sa, sb = a & 255, a >> 8
+        return lambda e: e + ((e >> sa) << sb)
     return lambda e: e ^ ((e >> a) & mask)
 
 
@@ -84,16 +88,65 @@ def exchange_cost(n, lr, esz, nt, x, fn, sstr):
     return tot / cnt / (2 if esz == 8 else 1)
 
 
+def linear_sides(n, lr, x, fn):
+    """Bit 0: every write of exchange x is phys(e(t,0,0)) + phys(e(0,u,f)); bit 1:
+    the same for every read -- the kernels then address the exchange as a
+    per-thread base plus compile-time offsets (ex_wr / ex_rd)."""
+    m = n.bit_length() - 1
+    r_ = 1 << lr
+    p_ = n // r_
+    sched = schedule(m, lr)
+    bits = 0
+    for bit, (p, kind) in enumerate(((x, "wr"), (x + 1, "rd"))):
+        s, k = sched[p]
+        rp = 1 << k
+        ns = 1 << s
+
+        def e_of(j, idx):
+            return j + idx * (n // rp) if kind == "rd" else (j >> s) * ns * rp + (j & (ns - 1)) + ns * idx
+        ok = all(fn(e_of(t + p_ * u, idx)) == fn(e_of(t, 0)) + fn(e_of(p_ * u, idx))
+                 for u in range(r_ // rp) for idx in range(rp) for t in range(p_))
+        bits |= ok << bit
+    return bits
+
+
+def nonlinear_sites(n, lr, x, fn):
+    """Accesses of exchange x (the Stockham write of pass x and the read of
+    pass x+1) whose physical slot is NOT the thread's first slot plus a
+    thread-independent constant: each of those costs the kernel address
+    arithmetic per access instead of an immediate offset."""
+    m = n.bit_length() - 1
+    r_ = 1 << lr
+    p_ = n // r_
+    sched = schedule(m, lr)
+    cnt = 0
+    for p, kind in ((x, "wr"), (x + 1, "rd")):
+        s, k = sched[p]
+        rp = 1 << k
+        ns = 1 << s
+
+        def e_of(j, idx):
+            return j + idx * (n // rp) if kind == "rd" else (j >> s) * ns * rp + (j & (ns - 1)) + ns * idx
+        for u in range(r_ // rp):
+            for idx in range(rp):
+                deltas = {fn(e_of(t + p_ * u, idx)) - fn(e_of(t, 0)) for t in range(p_)}
+                cnt += len(deltas) > 1
+    return cnt
+
+
 def plan(n, lr, esz, nt):
     m = n.bit_length() - 1
     sched = schedule(m, lr)
     p_ = n // (1 << lr)
     s_ = nt // p_
     lb = 5 if esz == 4 else 4
-    order = [(1, lr), (1, lb), (2, lr), (0, 0)] + [(1, a) for a in range(2, 11)] + [(2, a) for a in range(2, 11)]
+    order = ([(1, lr), (1, lb), (2, lr), (0, 0)] + [(1, a) for a in range(2, 11)]
+             + [(3, a | (b << 8)) for a in range(2, 12) for b in range(1, 6)] + [(2, a) for a in range(2, 11)])
     result = []
     for x in range(len(sched) - 1):
-        best = None
+        # every conflict-free layout, then the one with the fewest accesses
+        # that need per-access address arithmetic (ties: planner order)
+        best, free = None, []
         for kind, a in order:
             fn = phys_fn(kind, a, esz)
             span = fn(n - 1) + 1
@@ -104,10 +157,9 @@ def plan(n, lr, esz, nt):
                 if best is None or c < best[0] - 1e-9:
                     best = (c, kind, a, sstr)
                 if c <= 1.0 + 1e-9:
+                    free.append((nonlinear_sites(n, lr, x, fn), len(free), (c, kind, a, sstr)))
                     break
-            if best[0] <= 1.0 + 1e-9:
-                break
-        result.append(best)
+        result.append(min(free)[2] if free else best)
     return result
 
 
@@ -141,7 +193,7 @@ def shapes():
 def main():
     lines = [
         "// GENERATED by tools/plan_layouts.py -- shared-memory exchange layouts",
-        "// (per exchange x: kind 0 none / 1 pad A / 2 xor A, and the per-signal",
+        "// (per exchange x: kind 0 none / 1 pad A / 2 xor A / 3 shifted pad A | B << 8,\n// and the per-signal",
         "// stride), each checked bank-conflict free for both the Stockham write",
         "// and the next pass's read pattern.  Unlisted shapes use ExLayoutDefault.",
         "#pragma once",
@@ -150,6 +202,7 @@ def main():
         "    static constexpr bool planned = false;",
         "    __host__ __device__ static constexpr int kind(int) { return 1; }",
         "    __host__ __device__ static constexpr int arg(int) { return LR; }",
+        "    __host__ __device__ static constexpr int lin(int) { return 0; }",
         "    static constexpr int sstr = (1 << LOGN) + ((1 << LOGN) >> LR);",
         "};",
     ]
@@ -162,6 +215,7 @@ def main():
         worst = max(worst, max(r[0] for r in res))
         kinds = [r[1] for r in res] + [0] * (12 - len(res))
         args = [r[2] for r in res] + [0] * (12 - len(res))
+        lins = [linear_sides(n, lr, x, phys_fn(r[1], r[2], esz)) for x, r in enumerate(res)] + [0] * (12 - len(res))
         sstr = max(r[3] for r in res)
         costs = " ".join(f"{r[0]:.2f}" for r in res)
         lines += [
@@ -169,6 +223,7 @@ def main():
             "    static constexpr bool planned = true;",
             f"    __host__ __device__ static constexpr int kind(int x) {{ return {chain(kinds)}; }}",
             f"    __host__ __device__ static constexpr int arg(int x) {{ return {chain(args)}; }}",
+            f"    __host__ __device__ static constexpr int lin(int x) {{ return {chain(lins)}; }}",
             f"    static constexpr int sstr = {sstr};",
             "};",
         ]
