@@ -245,8 +245,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                     v[u * RP + r].x = lds_at<T>(inr, swz<T, N>(sl, e));                               \
                     v[u * RP + r].y = lds_at<T>(ini, swz<T, N>(sl, e));                               \
                 } else {                                                                             \
-                    v[u * RP + r].x = exr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];                    \
-                    v[u * RP + r].y = exi[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)];                    \
+                    v[u * RP + r].x = exr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];                    \
+                    v[u * RP + r].y = exi[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];                    \
                 }                                                                                    \
             }                                                                                        \
         }                                                                                            \
@@ -265,8 +265,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                 _Pragma("unroll") for (int f = 0; f < RP; ++f)                                       \
                 {                                                                                    \
                     const int e = base + ns * f;                                                     \
-                    exr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].x;              \
-                    exi[ex_phys<T, LOGN, LR, Sh::NT>(p, e)] = v[u * RP + brev(f, KP)].y;              \
+                    exr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, (t >> sp) * ns * RP + (t & (ns - 1)), ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f)] = v[u * RP + brev(f, KP)].x;              \
+                    exi[ex_wr<T, LOGN, LR, Sh::NT>(p, e, (t >> sp) * ns * RP + (t & (ns - 1)), ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f)] = v[u * RP + brev(f, KP)].y;              \
                 }                                                                                    \
             }                                                                                        \
             if (p == 0) {                                                                            \
@@ -327,8 +327,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                     v[d].x = lds_at<T>(inr, swz<T, N>(sl, e));                                        \
                     v[d].y = lds_at<T>(ini, swz<T, N>(sl, e));                                        \
                 } else {                                                                             \
-                    v[d].x = exr[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];                                 \
-                    v[d].y = exi[ex_phys<T, LOGN, LR, Sh::NT>(p, e)];                                 \
+                    v[d].x = exr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, (t >> sp) * ns * RP + (t & (ns - 1)), ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f)];                                 \
+                    v[d].y = exi[ex_wr<T, LOGN, LR, Sh::NT>(p, e, (t >> sp) * ns * RP + (t & (ns - 1)), ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f)];                                 \
                 }                                                                                    \
             }                                                                                        \
         }                                                                                            \
@@ -346,8 +346,8 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
                 _Pragma("unroll") for (int r = 0; r < RP; ++r)                                       \
                 {                                                                                    \
                     const int e = j + r * (N / RP);                                                  \
-                    exr[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].x;                    \
-                    exi[ex_phys<T, LOGN, LR, Sh::NT>(p - 1, e)] = v[u * RP + r].y;                    \
+                    exr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].x;                    \
+                    exi[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].y;                    \
                 }                                                                                    \
             }                                                                                        \
             if (q == 0) {                                                                            \
