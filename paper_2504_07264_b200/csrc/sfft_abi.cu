@@ -346,6 +346,22 @@ static bool pass_async_enabled()
 
 std::vector<Group> split_groups(int m)
 {
+    // developer knob for A/B runs: SFFT_PASS_SPLIT="8,7,7,6" (group sizes in
+    // launch order, each in [kPassMinL, kPassMaxL], summing to m)
+    if (const char *e = getenv("SFFT_PASS_SPLIT")) {
+        std::vector<Group> g;
+        int S = 0;
+        bool ok = true;
+        for (const char *c = e; *c && ok;) {
+            const int L = atoi(c);
+            ok = L >= kPassMinL && L <= kPassMaxL;
+            g.push_back({S, L});
+            S += L;
+            while (*c && *c != ',') ++c;
+            if (*c == ',') ++c;
+        }
+        if (ok && S == m) return g;
+    }
     const int maxl = pass_max_l();
     const int G = (m + maxl - 1) / maxl;
     std::vector<Group> g;
