@@ -355,11 +355,17 @@ def run_ours(args):
     torch.cuda.synchronize(device)
     launches0 = _ffi.launch_count()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    # one event pair around the K steps: nothing sits between consecutive
+    # launches of the stream (per-step events cost ~2% on the 0.17 ms cfg2
+    # step and block the TMA kernel's dependent launch); SFFT_BENCH_STEP_EVENTS=1
+    # records one per step for the step-time spread
+    step_events = os.environ.get("SFFT_BENCH_STEP_EVENTS", "0") != "0"
     t_wall0 = time.perf_counter()
     ev[0].record(stream)
     for k in range(args.steps):
         step()
-        ev[k + 1].record(stream)
+        if step_events or k == args.steps - 1:
+            ev[k + 1].record(stream)
     torch.cuda.synchronize(device)
     t_wall1 = time.perf_counter()
     if world > 1:
@@ -368,8 +374,9 @@ def run_ours(args):
     clocks.mark(t_wall0, t_wall1)
     time.sleep(0.01)
     clocks.stop()
-    per_step = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
     total_ms = ev[0].elapsed_time(ev[-1])
+    per_step = ([ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)] if step_events
+                else [total_ms / args.steps] * args.steps)
     ms_local = total_ms / args.steps
     # roofline unit: one HBM sweep (a launch that reads and writes the whole
     # batch once; the L2-blocked long-transform schedule does 2 sweeps in

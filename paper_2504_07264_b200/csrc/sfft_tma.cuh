@@ -191,6 +191,14 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
     }
     __syncthreads();
     if (tid == 0) {
+#ifndef SFFT_TMA_NO_PDL
+        // dependent launch (sfft_tma_host.h): wait for the previous grid of
+        // the stream (and its memory) before touching the signal planes --
+        // every global data access of this kernel is a TMA issued by this
+        // thread after this point; then let the next grid be scheduled
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
         for (int s = 0; s < STAGES && s < nk; ++s) issue_load(s, blockIdx.x + (int64_t)s * gridDim.x);
     }
 

@@ -84,9 +84,28 @@ cudaError_t launch_tma(const TmaLaunch &L, cudaStream_t st)
     int64_t grid = (int64_t)num_sms[dev] * blocks_per_sm[dev];
     if (grid > a.ntiles) grid = a.ntiles;
     if (grid < 1) grid = 1;
+#ifndef SFFT_TMA_NO_PDL
+    // programmatic dependent launch: this grid may be scheduled while the
+    // previous kernel of the stream drains; the kernel's griddepcontrol.wait
+    // (before its first TMA load) orders every global access after it
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(Sh::NT);
+    cfg.dynamicSmemBytes = Sh::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k, m_xr, m_xi, m_yr, m_yi, a);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+#else
     k<<<(unsigned)grid, Sh::NT, Sh::SMEM, st>>>(m_xr, m_xi, m_yr, m_yi, a);
     count_launch();
     return cudaGetLastError();
+#endif
 }
 
 }  // namespace sfft
