@@ -55,8 +55,6 @@ extern "C" {
 #define SFFT_KERNEL_LDG 1   /* per-thread global loads/stores (any stride/alignment, interleaved) */
 #define SFFT_KERNEL_TMA 2   /* require the TMA kernel (planar, 16-byte aligned rows and strides) */
 #define SFFT_KERNEL_PASS 3  /* reported by sfft_plan_info for the multi-launch path (log2n > 12) */
-#define SFFT_KERNEL_PAIR 4  /* fp32 planar: two signals per thread, packed across the pair (batch >= 2;
-                               odd batches pad the last pair, other layouts take the LDG kernel) */
 
 /* plan limit, transform.py:32 (MAX_PLAN_M) */
 #define SFFT_MAX_LOG2N 30
@@ -99,11 +97,8 @@ int sfft_plan_info(const sfft_plan *plan, int *log2n, int *dtype,
 
 /* The launch schedule exec uses for `batch` rows (interleaved != 0: the
  * interleaved layout): kernel launches per exec, and HBM sweeps per exec --
- * passes that read and write the whole signal once.  One launch per sweep,
- * except the opt-in (environment SFFT_BLOCKED=1) L2-blocked schedule of one
- * long DIT transform (batch 1, planar, log2n >= 23): two sweeps (a four-step split, block by block with the
- * intermediate of each block kept in L2) of many launches.  No reference
- * analogue (introspection, used for the roofline unit). */
+ * passes that read and write the whole signal once (one launch per sweep).
+ * No reference analogue (introspection, used for the roofline unit). */
 int sfft_exec_schedule(const sfft_plan *plan, int64_t batch, int interleaved,
                        int *launches, int *sweeps);
 
@@ -152,6 +147,10 @@ int sfft_dist_plan_destroy(sfft_dist_plan *plan);
 int sfft_dist_layout(const sfft_dist_plan *plan, int64_t *local_elems,
                      int *log2n1, int64_t *segment_elems);
 int sfft_dist_workspace_bytes(const sfft_dist_plan *plan, size_t *bytes);
+/* Pass-kernel launches of phase 0 and phase 1 (each launch reads and writes
+ * the rank's N/G elements of both planes once: the HBM sweep count). */
+int sfft_dist_schedule(const sfft_dist_plan *plan, int *launches_phase0,
+                       int *launches_phase1);
 int sfft_dist_exec_phase(const sfft_dist_plan *plan, int phase,
                          const void *x_re, const void *x_im, void *y_re,
                          void *y_im, int direction, void *workspace,

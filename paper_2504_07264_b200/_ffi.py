@@ -18,7 +18,7 @@ SFFT_F32, SFFT_F64 = 0, 1
 SFFT_DIT, SFFT_DIF = 0, 1
 SFFT_FORWARD, SFFT_INVERSE = -1, 1
 SFFT_MAX_LOG2N = 30
-SFFT_KERNEL_AUTO, SFFT_KERNEL_LDG, SFFT_KERNEL_TMA, SFFT_KERNEL_PASS, SFFT_KERNEL_PAIR = 0, 1, 2, 3, 4
+SFFT_KERNEL_AUTO, SFFT_KERNEL_LDG, SFFT_KERNEL_TMA, SFFT_KERNEL_PASS = 0, 1, 2, 3
 ABI_VERSION = 1
 
 # every symbol include/splitfft_b200.h declares: name -> (restype, argtypes)
@@ -43,6 +43,7 @@ SIGNATURES = {
     "sfft_dist_plan_destroy": (_I, [_P]),
     "sfft_dist_layout": (_I, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I), ctypes.POINTER(_I64)]),
     "sfft_dist_workspace_bytes": (_I, [_P, ctypes.POINTER(ctypes.c_size_t)]),
+    "sfft_dist_schedule": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
     "sfft_dist_exec_phase": (_I, [_P, _I, _P, _P, _P, _P, _I, _P, _P]),
     "sfft_dist_exec_phase0_p2p": (_I, [_P, _P, _P, ctypes.POINTER(_P), ctypes.POINTER(_P), _I, _I, _P, _P]),
 }

@@ -18,12 +18,6 @@
 #include <thread>
 #include <utility>
 
-#ifndef SFFT_BLOCK_MIN_M_DEFAULT
-#define SFFT_BLOCK_MIN_M_DEFAULT 23
-#endif
-#ifndef SFFT_PASS_ASYNC_DEFAULT
-#define SFFT_PASS_ASYNC_DEFAULT 0
-#endif
 #include <vector>
 
 #include "../../include/splitfft_b200.h"
@@ -31,7 +25,6 @@
 #include "sfft_launch.h"
 #include "sfft_pass.cuh"
 #include "sfft_tma_host.h"
-#include "sfft_pass_tma_host.h"
 
 #include <mutex>
 
@@ -141,7 +134,6 @@ struct sfft_plan {
     int log2n = 0, dtype = 0, algo = 0, device = 0, lr = 0;
     int kernel = SFFT_KERNEL_AUTO;  // fused-path kernel family
     int lr_tma = -1;                // radix of the TMA kernel (-1: none)
-    int lr_pair = -1;               // radix of the fp32 pair kernel (-1: none)
     int lr_ldg_il = 0;              // radix of the interleaved LDG kernel
     bool pre = false;               // fp32: fetch pass base factors up front
     // fused path
@@ -153,10 +145,6 @@ struct sfft_plan {
     int coarse_log = 0;
     double2 *d_fine = nullptr;
     std::vector<Group> groups;
-    // L2-blocked schedule: worker streams, created on first use
-    static constexpr int kWorkers = 4;
-    cudaStream_t wst[kWorkers] = {};
-    std::mutex wmu;
 };
 
 namespace {
@@ -244,8 +232,6 @@ void free_plan(sfft_plan *p)
     if (p->d_top) cudaFree(p->d_top);
     if (p->d_coarse) cudaFree(p->d_coarse);
     if (p->d_fine) cudaFree(p->d_fine);
-    for (cudaStream_t w : p->wst)
-        if (w) cudaStreamDestroy(w);
     delete p;
 }
 
@@ -274,74 +260,6 @@ static std::vector<Group> split_range(int S0, int stages)
         S += L;
     }
     return g;
-}
-
-// L2-blocked schedule for one long DIT transform (batch 1, planar), the
-// four-step split done inside one GPU: phase A runs stages 1..TA (TA =
-// floor(m/2)) column block by column block, phase B stages TA+1..m block by
-// block of the low TA index bits.  Inside a phase, consecutive launches of
-// one block hand over a block-sized scratch that stays in L2 (the 126 MB L2
-// holds a 32 MB block), so HBM sees two sweeps over the signal instead of
-// one per group.  The tile enumeration and the scratch addressing are the
-// sharded transform's (sfft_dist_*): the block id is a field of the
-// sub-problem index (jb bits at jpos) that the scratch maps squeeze out.
-struct Blocked {
-    bool on = false;
-    int TA = 0, bA = 0, bB = 0;   // phase split; log2 (columns | low-index values) per block
-    std::vector<Group> ga, gb;
-};
-
-static Blocked blocked_schedule(const sfft_plan *p, int64_t batch, bool il)
-{
-    Blocked b;
-    const int m = p->log2n;
-    if (il || batch != 1 || p->algo != SFFT_DIT || m <= kFusedMaxLog) return b;
-    // opt-in (SFFT_BLOCKED=1): measured slower on N = 2^28 fp32 (4.6 ms with
-    // 4 worker streams, 6.1 ms on one stream, vs 3.6 ms for the 4-sweep
-    // schedule): a 32 MB block launch is too short to reach steady state,
-    // and the pass kernel is closer to issue-bound than HBM-bound
-    const char *e = getenv("SFFT_BLOCKED");
-    if (!e || atoi(e) == 0) return b;
-    const char *mm = getenv("SFFT_BLOCK_MIN_M");
-    if (m < (mm ? atoi(mm) : SFFT_BLOCK_MIN_M_DEFAULT)) return b;
-    b.TA = m / 2;
-    b.ga = split_range(0, b.TA);
-    b.gb = split_range(b.TA, m - b.TA);
-    if (b.ga.size() < 2 || b.gb.size() < 2) return b;   // one launch per phase: nothing to hand over
-    // complex elements per block: 2^22 fp32 / 2^21 fp64 (32 MB per block)
-    const char *bl = getenv("SFFT_BLOCK_LOG");
-    const int target = bl ? atoi(bl) : (p->dtype == SFFT_F32 ? 22 : 21);
-    // 5 <= b (a tile's 32 sub-problems stay contiguous), jb = TA - b >= 3
-    // (4 worker streams x 2 scratch slots fit the workspace)
-    auto clampb = [&](int v) { return v < 5 ? 5 : (v > b.TA - 3 ? b.TA - 3 : v); };
-    b.bA = clampb(target - (m - b.TA));
-    b.bB = clampb(target - (m - b.TA));
-    b.on = true;
-    return b;
-}
-
-static bool l2_discard_enabled()
-{
-    const char *e = getenv("SFFT_L2_DISCARD");
-    return e ? atoi(e) != 0 : true;
-}
-
-// The TMA-pipelined pass kernel (sfft_pass_tma.cuh) is correct (parity tests
-// run it with SFFT_PASS_TMA=1) but measured slower than the LDG pass kernel
-// (N = 2^28 fp32: 6.25 vs 3.83 ms -- twiddle latency with 8-16 warps per SM),
-// so it is opt-in until it is pipelined further.
-static bool pass_tma_enabled()
-{
-    const char *e = getenv("SFFT_PASS_TMA");
-    return e && atoi(e) != 0;
-}
-
-// The persistent cp.async-pipelined pass kernel (sfft_pass_async.cuh) for
-// the planar groups with S > 0.  SFFT_PASS_ASYNC=0/1 overrides the default.
-static bool pass_async_enabled()
-{
-    const char *e = getenv("SFFT_PASS_ASYNC");
-    return e ? atoi(e) != 0 : SFFT_PASS_ASYNC_DEFAULT;
 }
 
 std::vector<Group> split_groups(int m)
@@ -388,105 +306,6 @@ int validate_exec(const sfft_plan *p, int64_t batch, int64_t is, int64_t os, int
     return SFFT_OK;
 }
 
-int exec_blocked(const sfft_plan *pc, const Blocked &bp, const void *x0, const void *x1, void *y0, void *y1,
-                 bool inv, double scale, void *workspace, cudaStream_t st)
-{
-    sfft_plan *p = const_cast<sfft_plan *>(pc);   // worker streams only
-    const int m = p->log2n;
-    const int64_t n = int64_t(1) << m;
-    const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
-    const int jbA = bp.TA - bp.bA, jbB = bp.TA - bp.bB;
-    constexpr int NW = sfft_plan::kWorkers;
-    // blocks run on NW worker streams (block R on stream R % NW), so that the
-    // launches of different blocks overlap; workspace: the phase A -> B
-    // intermediate (2 planes of N), then per worker two scratch slots of 2
-    // planes (each <= N / (2 NW): jb >= 1 + log2 NW)
-    char *ws = (char *)workspace;
-    void *X[2] = {ws, ws + n * esz};
-    const size_t blk = (size_t)(n >> (jbA < jbB ? jbA : jbB)) * esz;
-    char *sb = ws + 2 * n * esz;
-    const bool disc = l2_discard_enabled();
-    std::lock_guard<std::mutex> lk(p->wmu);
-    for (int w = 0; w < NW; ++w)
-        if (!p->wst[w]) {
-            cudaError_t e = cudaStreamCreateWithFlags(&p->wst[w], cudaStreamNonBlocking);
-            if (e != cudaSuccess) return cuda_fail(e, "creating worker streams");
-        }
-    cudaEvent_t ev[NW + 1];
-    for (int w = 0; w <= NW; ++w) {
-        cudaError_t e = cudaEventCreateWithFlags(&ev[w], cudaEventDisableTiming);
-        if (e != cudaSuccess) return cuda_fail(e, "creating events");
-    }
-    int rc = SFFT_OK;
-    for (int ph = 0; ph < 2 && rc == SFFT_OK; ++ph) {
-        const std::vector<Group> &g = ph ? bp.gb : bp.ga;
-        const int jb = ph ? jbB : jbA, bl = ph ? bp.bB : bp.bA;
-        const int G = (int)g.size();
-        const int nw = (1 << jb) < NW ? (1 << jb) : NW;
-        cudaEventRecord(ev[NW], st);   // fork
-        for (int w = 0; w < nw; ++w) cudaStreamWaitEvent(p->wst[w], ev[NW], 0);
-        for (int R = 0; R < (1 << jb) && rc == SFFT_OK; ++R) {
-            const int w = R % nw;
-            char *slot[2] = {sb + (size_t)w * 4 * blk, sb + (size_t)w * 4 * blk + 2 * blk};
-            for (int i = 0; i < G; ++i) {
-                const Group gr = g[i];
-                const bool first = i == 0, last = i == G - 1;
-                PassLaunchFn fn = pass_launcher(p->dtype, gr.L);
-                if (!fn) {
-                    rc = fail(SFFT_EINVAL, "no pass kernel for L=%d", gr.L);
-                    break;
-                }
-                PassArgs a;
-                memset(&a, 0, sizeof a);
-                char *src = slot[(i + 1) % 2], *dst = slot[i % 2];
-                a.x0 = first ? (ph ? X[0] : x0) : src;
-                a.x1 = first ? (ph ? X[1] : x1) : src + blk;
-                a.y0 = last ? (ph ? y0 : X[0]) : dst;
-                a.y1 = last ? (ph ? y1 : X[1]) : dst + blk;
-                a.batch = 1;
-                a.in_stride = a.out_stride = n;
-                a.m = m;
-                a.S = gr.S;
-                a.swap_in = ph == 0 && first && inv;
-                a.swap_out = ph == 1 && last && inv;
-                a.scale = (ph == 1 && last) ? scale : 1.0;
-                a.tw = p->d_tw;
-                a.tw_cat_top = p->cat_top;
-                a.tw_top_tab = p->d_top;
-                a.coarse = p->d_coarse;
-                a.coarse_log = p->coarse_log;
-                a.fine = p->d_fine;
-                a.jb = jb;
-                a.jrank = R;
-                const AddrMap id = {0, 0, -1, m};
-                if (ph == 0) {   // block field: bits [S + bl, S + TA) of the sub-problem index
-                    a.jpos = gr.S + bl;
-                    a.in_map = first ? id : AddrMap{jb, gr.S + bl, -1, m - jb};
-                    a.out_map = last ? id : AddrMap{jb, gr.S + gr.L + bl, -1, m - jb};
-                } else {         // block field: bits [bl, TA) of the low index
-                    a.jpos = bl;
-                    a.in_map = first ? id : AddrMap{jb, bl, -1, m - jb};
-                    a.out_map = last ? id : AddrMap{jb, bl, -1, m - jb};
-                }
-                a.keep_out = !last;
-                a.discard_in = !first && disc;
-                const int64_t grid = ((n >> gr.L) >> jb) / pass_tile(p->dtype, gr.L);
-                cudaError_t e = fn(a, false, false, false, grid, p->wst[w]);
-                if (e != cudaSuccess) {
-                    rc = cuda_fail(e, "pass kernel launch (blocked)");
-                    break;
-                }
-            }
-        }
-        for (int w = 0; w < nw; ++w) {   // join
-            cudaEventRecord(ev[w], p->wst[w]);
-            cudaStreamWaitEvent(st, ev[w], 0);
-        }
-    }
-    for (int w = 0; w <= NW; ++w) cudaEventDestroy(ev[w]);
-    return rc;
-}
-
 int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, void *y1, bool il,
                 int64_t batch, int64_t is, int64_t os, int direction, void *workspace, void *stream)
 {
@@ -508,25 +327,6 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         const bool aligned = ((uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)y0 | (uintptr_t)y1) % 16 == 0 &&
                              ((size_t)is * esz) % 16 == 0 && ((size_t)os * esz) % 16 == 0 &&
                              batch < (int64_t(1) << 31);
-        if (!il && p->lr_pair >= 0 && batch >= 2) {
-            FusedLaunchFn pf = fused_pair_launcher(m, p->lr_pair, p->algo == SFFT_DIF);
-            if (pf) {
-                FusedArgs a;
-                a.x0 = x0;
-                a.x1 = x1;
-                a.y0 = y0;
-                a.y1 = y1;
-                a.tw = p->d_tw;
-                a.batch = batch;
-                a.in_stride = is;
-                a.out_stride = os;
-                a.inverse = inv ? 1 : 0;
-                a.scale = scale;
-                cudaError_t e = pf(a, p->algo == SFFT_DIF, false, st);
-                if (e != cudaSuccess) return cuda_fail(e, "pair kernel launch");
-                return SFFT_OK;
-            }
-        }
         if (!il && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG && aligned) {
             TmaLaunchFn tf = tma_launcher(p->dtype, m, p->lr_tma, p->algo == SFFT_DIF, p->pre);
             if (tf) {
@@ -571,10 +371,6 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
 
     // multi-launch schedule: groups in order (DIT) or reverse order (DIF)
     if (!workspace) return fail(SFFT_EINVAL, "log2n=%d needs a workspace (sfft_workspace_bytes)", m);
-    {
-        const Blocked bp = blocked_schedule(p, batch, il);
-        if (bp.on) return exec_blocked(p, bp, x0, x1, y0, y1, inv, scale, workspace, st);
-    }
     const int64_t n = int64_t(1) << m;
     const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
     const int G = (int)p->groups.size();
@@ -624,47 +420,6 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         a.fine = p->d_fine;
         a.jb = 0;
         a.in_map.b = a.out_map.b = 0;
-        // groups after the first stage block: TMA-pipelined kernel when the
-        // planes are 16-byte aligned with 16-byte row strides
-        const bool planar_here = !((first || last) && il);
-        const bool al = (((uintptr_t)a.x0 | (uintptr_t)a.x1 | (uintptr_t)a.y0 | (uintptr_t)a.y1) % 16 == 0) &&
-                        ((size_t)a.in_stride * esz) % 16 == 0 && ((size_t)a.out_stride * esz) % 16 == 0 &&
-                        batch < (int64_t(1) << 31);
-        PassTmaLaunchFn tf = (pass_tma_enabled() && gr.S > 0 && planar_here && al && p->kernel != SFFT_KERNEL_LDG)
-                                 ? pass_tma_launcher(p->dtype, gr.L, p->algo == SFFT_DIF) : nullptr;
-        if (tf) {
-            PassTmaLaunch Lc;
-            Lc.x_re = a.x0;
-            Lc.x_im = a.x1;
-            Lc.y_re = a.y0;
-            Lc.y_im = a.y1;
-            Lc.batch = batch;
-            Lc.in_stride = a.in_stride;
-            Lc.out_stride = a.out_stride;
-            if (a.swap_in) std::swap(Lc.x_re, Lc.x_im);
-            if (a.swap_out) std::swap(Lc.y_re, Lc.y_im);
-            memset(&Lc.a, 0, sizeof Lc.a);
-            Lc.a.m = m;
-            Lc.a.S = gr.S;
-            Lc.a.scale_out = a.swap_out;
-            Lc.a.scale = a.scale;
-            Lc.a.tw = a.tw;
-            Lc.a.tw_cat_top = a.tw_cat_top;
-            Lc.a.tw_top_tab = a.tw_top_tab;
-            Lc.a.coarse = a.coarse;
-            Lc.a.coarse_log = a.coarse_log;
-            Lc.a.fine = a.fine;
-            cudaError_t e = tf(Lc, st);
-            if (e != cudaSuccess) return cuda_fail(e, "TMA pass kernel launch");
-            continue;
-        }
-        PassAsyncLaunchFn af = (pass_async_enabled() && gr.S > 0 && planar_here && p->kernel != SFFT_KERNEL_LDG)
-                                   ? pass_async_launcher(p->dtype, gr.L, p->algo == SFFT_DIF, false) : nullptr;
-        if (af) {
-            cudaError_t e = af(a, st);
-            if (e != cudaSuccess) return cuda_fail(e, "async pass kernel launch");
-            continue;
-        }
         const int64_t grid = batch * ((n >> gr.L) / TJ);
         if (grid > 0x7fffffffLL)
             return fail(SFFT_ECAPACITY, "batch %lld x N=2^%d exceeds one launch; split the batch", (long long)batch, m);
@@ -724,8 +479,7 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
     if (dtype != SFFT_F32 && dtype != SFFT_F64) return fail(SFFT_EINVAL, "unknown dtype %d", dtype);
     const int pre_pref = (kernel >> 4) & 3;   // 0 auto, 1 off, 2 on
     kernel &= 0xf;
-    if ((kernel != SFFT_KERNEL_AUTO && kernel != SFFT_KERNEL_LDG && kernel != SFFT_KERNEL_TMA &&
-         kernel != SFFT_KERNEL_PAIR) || pre_pref == 3)
+    if ((kernel != SFFT_KERNEL_AUTO && kernel != SFFT_KERNEL_LDG && kernel != SFFT_KERNEL_TMA) || pre_pref == 3)
         return fail(SFFT_EINVAL, "unknown kernel family %d", kernel);
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -748,11 +502,7 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
         bool auto_pre = false;
         int auto_lr = 0, auto_family = 0;
         auto_choice(dtype, log2n, &auto_family, &auto_lr, &auto_pre);
-        const bool auto_tma = auto_family == 1, auto_pair = auto_family == 2;
-        if (kernel == SFFT_KERNEL_PAIR && (dtype != SFFT_F32 || log2n < 1)) {
-            delete p;
-            return fail(SFFT_EINVAL, "the pair kernel is fp32 only (log2n >= 1)");
-        }
+        const bool auto_tma = auto_family == 1;
         p->pre = pre_pref == 2 || (pre_pref == 0 && kernel == SFFT_KERNEL_AUTO && log2_radix <= 0 && auto_pre);
         int lr;
         if (log2_radix > 0) lr = log2_radix;
@@ -770,13 +520,6 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
         const bool want_tma = kernel == SFFT_KERNEL_TMA ||
                               (kernel == SFFT_KERNEL_AUTO && (log2_radix > 0 || auto_tma));
         if (want_tma && tma_launcher(dtype, log2n, lr, false, p->pre)) p->lr_tma = lr;
-        const bool want_pair = kernel == SFFT_KERNEL_PAIR ||
-                               (kernel == SFFT_KERNEL_AUTO && log2_radix <= 0 && auto_pair);
-        if (want_pair && fused_pair_launcher(log2n, lr, false)) p->lr_pair = lr;
-        if (kernel == SFFT_KERNEL_PAIR && p->lr_pair < 0) {
-            delete p;
-            return fail(SFFT_EINVAL, "no pair kernel for log2n=%d radix=2^%d", log2n, lr);
-        }
         if (kernel == SFFT_KERNEL_TMA && p->lr_tma < 0) {
             delete p;
             return fail(SFFT_EINVAL, "no TMA kernel for log2n=%d radix=2^%d", log2n, lr);
@@ -819,8 +562,7 @@ int sfft_plan_info(const sfft_plan *p, int *log2n, int *dtype, int *algorithm, i
                    int *log2_radix, int *kernel)
 {
     if (kernel && p)
-        *kernel = p->lr_pair >= 0  ? SFFT_KERNEL_PAIR
-                  : p->lr_tma >= 0 ? SFFT_KERNEL_TMA
+        *kernel = p->lr_tma >= 0 ? SFFT_KERNEL_TMA
                                    : (p->log2n <= kFusedMaxLog ? SFFT_KERNEL_LDG : SFFT_KERNEL_PASS);
     if (!p) return fail(SFFT_EINVAL, "plan is NULL");
     if (log2n) *log2n = p->log2n;
@@ -837,16 +579,8 @@ int sfft_exec_schedule(const sfft_plan *p, int64_t batch, int interleaved, int *
     if (!p) return fail(SFFT_EINVAL, "plan is NULL");
     if (batch < 0) return fail(SFFT_EINVAL, "batch must be >= 0, got %lld", (long long)batch);
     int nl = 1, ns = 1;
-    if (p->log2n > kFusedMaxLog) {
-        const Blocked bp = blocked_schedule(p, batch, interleaved != 0);
-        if (bp.on) {
-            nl = (int)bp.ga.size() << (bp.TA - bp.bA);
-            nl += (int)bp.gb.size() << (bp.TA - bp.bB);
-            ns = 2;
-        } else {
-            nl = ns = (int)p->groups.size();
-        }
-    }
+    (void)interleaved;
+    if (p->log2n > kFusedMaxLog) nl = ns = (int)p->groups.size();
     if (launches) *launches = nl;
     if (sweeps) *sweeps = ns;
     return SFFT_OK;
@@ -940,6 +674,14 @@ int sfft_dist_layout(const sfft_dist_plan *d, int64_t *local_elems, int *log2n1,
     if (local_elems) *local_elems = n >> d->logg;
     if (log2n1) *log2n1 = d->L1;
     if (segment_elems) *segment_elems = n >> (2 * d->logg);
+    return SFFT_OK;
+}
+
+int sfft_dist_schedule(const sfft_dist_plan *d, int *launches_phase0, int *launches_phase1)
+{
+    if (!d) return fail(SFFT_EINVAL, "plan is NULL");
+    if (launches_phase0) *launches_phase0 = (int)d->ga.size();
+    if (launches_phase1) *launches_phase1 = (int)d->gb.size();
     return SFFT_OK;
 }
 
@@ -1044,12 +786,6 @@ static int dist_exec(const sfft_dist_plan *d, int phase, const void *x_re, const
             a.jpos = L1 - b;
             a.in_map = {b, L1 - b, -1, m - b};
             a.out_map = {b, L1 - b, -1, m - b};
-        }
-        PassAsyncLaunchFn af = (pass_async_enabled() && gr.S > 0) ? pass_async_launcher(p->dtype, gr.L, false, true) : nullptr;
-        if (af) {
-            cudaError_t e = af(a, (cudaStream_t)stream);
-            if (e != cudaSuccess) return cuda_fail(e, "async pass kernel launch (sharded)");
-            continue;
         }
         const int64_t grid = ((n >> gr.L) >> b) / TJ;
         cudaError_t e = fn(a, false, false, false, grid, (cudaStream_t)stream);

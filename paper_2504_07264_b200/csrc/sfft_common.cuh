@@ -33,6 +33,29 @@ __host__ __device__ constexpr int brev(int f, int bits)
 
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 
+template <int V> struct IntC { static constexpr int value = V; };
+
+// f(IntC<g>) for a runtime g in [G, N_): compile-time register indices for
+// code specialised per (warp-uniform) group position.
+template <int G, int N_, typename F>
+__device__ __forceinline__ void with_g(int g, F &&f)
+{
+    if constexpr (G < N_) {
+        if (g == G) f(IntC<G>{});
+        else with_g<G + 1, N_>(g, f);
+    }
+}
+
+// f(IntC<0>), f(IntC<1>), ..., f(IntC<N_-1>) (compile-time loop)
+template <int I, int N_, typename F>
+__device__ __forceinline__ void static_for(F &&f)
+{
+    if constexpr (I < N_) {
+        f(IntC<I>{});
+        static_for<I + 1, N_>(f);
+    }
+}
+
 __device__ __forceinline__ void cmul(float ar, float ai, float br, float bi, float &cr, float &ci)
 {
     cr = __fmaf_rn(ar, br, -__fmul_rn(ai, bi));
@@ -324,9 +347,13 @@ __device__ __forceinline__ vec2_t<T> stage_factor(int t, int f, int i, bool firs
 // tests/test_schedule_model.py (a numpy restatement of this index map).
 // TRIV = false promises gs >= 1 and no trivial factors to skip (every pass
 // group after the first), which removes the per-stage kind tests.
+// `hw` (optional): every factor of the K stages already in registers, stage
+// t's 2^(t-1) factors at hw[2^(t-1) - 1 + f] (the persistent kernels load
+// them once per thread for all tiles -- the factors depend on the thread's
+// column only -- so no table read sits in the tile loop).
 template <typename T, int K, bool TRIV = true, bool PACK = true, typename TW>
 __device__ __forceinline__ void dit_stages(vec2_t<T> *v, int gs, typename TW::index_t cbase, const TW &tw,
-                                           const vec2_t<T> *pre = nullptr)
+                                           const vec2_t<T> *pre = nullptr, const vec2_t<T> *hw = nullptr)
 {
     const bool first = TRIV && gs == 0;   // first pass: every factor is a compile-time constant
 #pragma unroll
@@ -345,7 +372,7 @@ __device__ __forceinline__ void dit_stages(vec2_t<T> *v, int gs, typename TW::in
                            : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w, wq;
             if (kind == 3) {
-                w = stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                w = (hw && !first) ? hw[(1 << (t - 1)) - 1 + f] : stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
                 wq = wquad<T>(w);
             }
 #pragma unroll
@@ -371,7 +398,7 @@ __device__ __forceinline__ void dit_stages(vec2_t<T> *v, int gs, typename TW::in
 // register map run backwards.
 template <typename T, int K, bool TRIV = true, bool PACK = true, typename TW>
 __device__ __forceinline__ void dif_stages(vec2_t<T> *v, int gs, typename TW::index_t cbase, const TW &tw,
-                                           const vec2_t<T> *pre = nullptr)
+                                           const vec2_t<T> *pre = nullptr, const vec2_t<T> *hw = nullptr)
 {
     const bool first = TRIV && gs == 0;
 #pragma unroll
@@ -389,7 +416,7 @@ __device__ __forceinline__ void dif_stages(vec2_t<T> *v, int gs, typename TW::in
                            : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w, wq;
             if (kind == 3) {
-                w = stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                w = (hw && !first) ? hw[(1 << (t - 1)) - 1 + f] : stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
                 wq = wquad<T>(w);
             }
 #pragma unroll

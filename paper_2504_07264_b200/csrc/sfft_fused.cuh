@@ -21,7 +21,6 @@
 
 namespace sfft {
 
-template <int V> struct IntC { static constexpr int value = V; };
 
 struct FusedArgs {
     const void *x0, *x1;   // planar: re, im planes; interleaved: x0 = pairs
@@ -171,15 +170,6 @@ struct LastX {
 #endif
     static constexpr int GSTRIDE = Sh::P / RPL;      // threads per group position
 };
-
-template <int G, int N_, typename F>
-__device__ __forceinline__ void with_g(int g, F &&f)
-{
-    if constexpr (G < N_) {
-        if (g == G) f(IntC<G>{});
-        else with_g<G + 1, N_>(g, f);
-    }
-}
 
 // ---- DIT pass p -----------------------------------------------------------
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>

@@ -9,7 +9,6 @@ namespace sfft {
 struct FusedArgs;
 struct PassArgs;
 struct TmaLaunch;
-struct PassTmaLaunch;
 
 // Launch one fused kernel (N = 2^logn <= 4096) over a.batch rows.
 using FusedLaunchFn = cudaError_t (*)(const FusedArgs &a, bool dif, bool interleaved, cudaStream_t st);
@@ -20,12 +19,6 @@ using PassLaunchFn = cudaError_t (*)(const PassArgs &a, bool dif, bool il_in, bo
 // Launch the persistent TMA-fed fused kernel (planar, 16-byte aligned rows).
 using TmaLaunchFn = cudaError_t (*)(const TmaLaunch &L, cudaStream_t st);
 
-// Launch the TMA-pipelined pass kernel (groups with S > 0, planar rows).
-using PassTmaLaunchFn = cudaError_t (*)(const PassTmaLaunch &L, cudaStream_t st);
-
-// Launch the persistent cp.async-pipelined pass kernel (groups with S > 0,
-// planar rows); the launcher sizes the grid to the resident CTAs.
-using PassAsyncLaunchFn = cudaError_t (*)(const PassArgs &a, cudaStream_t st);
 
 constexpr int kFusedMaxLog = 12;
 constexpr int kMaxRadixLog = 5;
@@ -47,20 +40,8 @@ TmaLaunchFn tma_launcher(int dtype, int logn, int lr, bool dif, bool pre = false
 TmaLaunchFn tma_launcher_f32(int logn, int lr, bool dif, bool pre);
 TmaLaunchFn tma_launcher_f64(int logn, int lr, bool dif, bool pre);
 int tma_default_lr(int dtype, int logn);   // -1: no TMA config for this size
-// kernel=auto pick, 0 <= logn <= 12: family 0 = LDG fused, 1 = TMA, 2 = pair (fp32)
+// kernel=auto pick, 0 <= logn <= 12: family 0 = LDG fused, 1 = TMA
 void auto_choice(int dtype, int logn, int *family, int *lr, bool *pre);
-// fp32 planar fused kernel with two signals per thread (sfft_fused_pair.cuh);
-// bound to dif, ignores the (dif, il) arguments
-FusedLaunchFn fused_pair_launcher(int logn, int lr, bool dif);
-
-PassTmaLaunchFn pass_tma_launcher(int dtype, int L, bool dif);
-PassTmaLaunchFn pass_tma_launcher_f32(int L, bool dif);
-PassTmaLaunchFn pass_tma_launcher_f64(int L, bool dif);
-
-PassAsyncLaunchFn pass_async_launcher(int dtype, int L, bool dif, bool dist);
-PassAsyncLaunchFn pass_async_launcher_f32(int L, bool dif, bool dist);
-PassAsyncLaunchFn pass_async_launcher_f64(int L, bool dif, bool dist);
-
 void count_launch();
 
 }  // namespace sfft

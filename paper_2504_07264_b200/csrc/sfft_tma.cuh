@@ -38,6 +38,10 @@ struct TmaArgs {
     double scale;        // 1/N when the caller swapped the maps for the inverse
     int scale_out;
     const void *tw;
+    // OB == 0 (direct stores from the last register pass): output planes
+    // (already channel-swapped for the inverse), rows, row stride (elements)
+    void *y_re, *y_im;
+    int64_t batch, out_stride;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p)
@@ -93,7 +97,7 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 template <int N>
 __device__ __forceinline__ void bulk_wait_read()
 {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+    if constexpr (N >= 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -103,6 +107,8 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
 // Shape of the TMA kernel.  NT_REQ: requested threads per CTA (>= P).
+// OB = 0: the last register pass stores straight to global memory (no output
+// tile, no TMA store) -- frees OB*2*TILE bytes of shared memory per CTA.
 template <typename T, int LOGN, int LR_REQ, int NT_REQ, int STAGES, int OB>
 struct TmaShape {
     static constexpr int N = 1 << LOGN;
@@ -146,23 +152,26 @@ __device__ __forceinline__ void sts_at(unsigned char *base, uint32_t off, T v)
     *reinterpret_cast<T *>(base + off) = v;
 }
 
-template <typename T, int LOGN, int LR_REQ, bool DIF, int NT_REQ, int STAGES, int OB, bool PRE_T = false>
-__global__ void __launch_bounds__(TmaShape<T, LOGN, LR_REQ, NT_REQ, STAGES, OB>::NT)
-sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant__ CUtensorMap in_im,
-                const __grid_constant__ CUtensorMap out_re, const __grid_constant__ CUtensorMap out_im,
-                const TmaArgs a)
+template <typename T, int LOGN, int LR_REQ, bool DIF, int NT_REQ, int STAGES, int OB, bool PRE_T>
+__device__ __forceinline__ void tma_body(const CUtensorMap &in_re, const CUtensorMap &in_im,
+                                         const CUtensorMap &out_re, const CUtensorMap &out_im, const TmaArgs &a)
 {
     using Sh = TmaShape<T, LOGN, LR_REQ, NT_REQ, STAGES, OB>;
     constexpr int N = Sh::N, R = Sh::R, P = Sh::P, S = Sh::S, LR = Sh::LR, NPASS = Sh::NPASS,
                   TILE = Sh::TILE, SSTR = Sh::SSTR, W = Sh::W;
     extern __shared__ unsigned char smem_raw[];
-    // 1024-byte alignment for the 128B swizzle (see TMA_PACK for why the
-    // generic-pointer form is the default)
-#ifndef SFFT_TMA_LDS
-    unsigned char *smem = reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    // 1024-byte alignment for the 128B swizzle.  fp32 addresses shared
+    // memory through generic pointers (measured faster on cfg2, see TMA_PACK);
+    // fp64 keeps the shared window (LDS/STS: 0.864 -> 0.880 of the HBM peak on
+    // cfg3 fp64, profiles/r02a_ab_f64_tma.txt)
+#ifdef SFFT_TMA_LDS
+    constexpr bool kShWindow = true;
 #else
-    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    constexpr bool kShWindow = sizeof(T) == 8;
 #endif
+    unsigned char *smem = kShWindow
+        ? smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u)
+        : reinterpret_cast<unsigned char *>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     unsigned char *in_buf = smem + Sh::IN_OFF;      // [STAGES][2 planes][TILE]
     unsigned char *out_buf = smem + Sh::OUT_OFF;    // [OB][2][TILE]
     T *ex = reinterpret_cast<T *>(smem + Sh::EX_OFF);
@@ -220,191 +229,336 @@ sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant
             }
         }
     }
+    // fp64 (table factors, bit-exact contract): every factor of passes >= 1
+    // depends on the thread's column only, so the whole per-thread set is
+    // loaded once here and lives in registers for all tiles (fp64 N = 1024
+    // radix 8: 18 complex factors) -- the tile loop issues no table reads,
+    // which took ~40% of the L1 wavefronts of the per-use loads.  Virtual
+    // threads u > 0 whose column equals u = 0's share its slots.
+    constexpr bool HOIST = !FactorTw<T>::value && NPASS >= 2;
+    vec2_t<T> hw[NPASS][R];
+    if constexpr (HOIST) {
+#pragma unroll
+        for (int p = 1; p < NPASS; ++p) {
+            const int sp = p * LR;
+            const int kp = cmin(LR, LOGN - sp);
+            const int rp = 1 << kp, ns = 1 << sp;
+#pragma unroll
+            for (int u = 0; u < R / rp; ++u) {
+                if (u > 0 && ((P * u) & (ns - 1)) == 0) continue;
+                const int j = t + P * u;
+#pragma unroll
+                for (int tt = 1; tt <= kp; ++tt)
+#pragma unroll
+                    for (int f = 0; f < (1 << (tt - 1)); ++f)
+                        hw[p][u * (rp - 1) + (1 << (tt - 1)) - 1 + f] = tw.get(sp + tt, (j & (ns - 1)) + (f << sp));
+            }
+        }
+    }
     T *exr = ex + sl * SSTR;
     T *exi = ex + S * SSTR + sl * SSTR;
+    T *ygr = reinterpret_cast<T *>(a.y_re);
+    T *ygi = reinterpret_cast<T *>(a.y_im);
+
+    // Partial last exchange (as sfft_fused.cuh LastX): when the last DIT
+    // pass runs KPL < LR stages, the exchange before it only permutes values
+    // inside groups of RPL threads, so 1/RPL of each thread's values stay in
+    // registers (fp64 N = 1024 radix 8, passes 3+3+3+1: half of that
+    // exchange).  g = t / GSTRIDE is warp-uniform (GSTRIDE >= 32).
+    constexpr int KPL = LOGN - (NPASS - 1) * LR;
+    constexpr int RPL = 1 << KPL;
+#ifdef SFFT_NO_PARTIAL_EXCHANGE
+    constexpr bool PX = false;
+#else
+    constexpr bool PX = NPASS >= 2 && KPL < LR && P / RPL >= 32;
+#endif
+    constexpr int GSTRIDE = P / RPL;
+    const int g = t / GSTRIDE;
 
     for (int64_t k = 0; k < nk; ++k) {
         const int st = (int)(k % STAGES);
-        const int ob = (int)(k % OB);
+        const int ob = OB > 0 ? (int)(k % OB) : 0;
         const int64_t tile = blockIdx.x + k * gridDim.x;
         const unsigned char *inr = in_buf + (st * 2 + 0) * TILE;
         const unsigned char *ini = in_buf + (st * 2 + 1) * TILE;
         unsigned char *outr = out_buf + (ob * 2 + 0) * TILE;
         unsigned char *outi = out_buf + (ob * 2 + 1) * TILE;
+        const int64_t orow = tile * S + sl;   // OB == 0: this thread's output row
         mbar_wait(full + st, (uint32_t)((k / STAGES) & 1));
 
+        // input slot consumed (and, OB > 0, output buffer `ob` free): refill
+        auto release_input = [&]() {
+            if (tid == 0) bulk_wait_read<OB - 1>();
+            __syncthreads();
+            if (tid == 0 && k + STAGES < nk) issue_load(st, tile + (int64_t)STAGES * gridDim.x);
+        };
+        auto put = [&](int e, T re, T im) {
+            if (do_scale) {
+                re *= scale;
+                im *= scale;
+            }
+            if constexpr (OB == 0) {
+                if (orow < a.batch) {
+                    st_stream(ygr + orow * a.out_stride + e, re);
+                    st_stream(ygi + orow * a.out_stride + e, im);
+                }
+            } else {
+                sts_at<T>(outr, swz<T, N>(sl, e), re);
+                sts_at<T>(outi, swz<T, N>(sl, e), im);
+            }
+        };
+        // hoisted-factor slot of virtual thread u in pass p (u > 0 with u = 0's column shares it)
+        auto hwp = [&](int p, int u, int rp) -> const vec2_t<T> * {
+            const int ns = 1 << (p * LR);
+            return &hw[p][((u > 0 && ((P * u) & (ns - 1)) == 0) ? 0 : u) * (rp - 1)];
+        };
+
         if constexpr (!DIF) {
-            // ---------------- DIT ----------------
+            // ---------------- DIT: passes 0 .. NPASS-1 ----------------
+            static_for<0, NPASS>([&](auto PC) {
+                constexpr int p = decltype(PC)::value;
+                constexpr int sp = p * LR, KP = cmin(LR, LOGN - sp), RP = 1 << KP, U = R / RP, ns = 1 << sp;
+                constexpr bool FIRST = p == 0, LAST = p == NPASS - 1;
+                const int et = (t >> sp) * ns * RP + (t & (ns - 1));
+                // gather
+                if constexpr (FIRST) {
 #pragma unroll
-            for (int p = 0; p < NPASS; ++p) {
-                const int sp = p * LR;
-                const int kp = cmin(LR, LOGN - sp);
-#define SFFT_TMA_DIT(KP)                                                                              \
-    if constexpr (KP <= LR) if (kp == KP) {                                                          \
-        constexpr int RP = 1 << KP, U = R / RP;                                                      \
-        const int ns = 1 << sp;                                                                      \
-        _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
-        {                                                                                            \
-            const int j = t + P * u;                                                                 \
-            _Pragma("unroll") for (int r = 0; r < RP; ++r)                                           \
-            {                                                                                        \
-                const int e = j + r * (N / RP);                                                      \
-                if (p == 0) {                                                                        \
-                    v[u * RP + r].x = lds_at<T>(inr, swz<T, N>(sl, e));                               \
-                    v[u * RP + r].y = lds_at<T>(ini, swz<T, N>(sl, e));                               \
-                } else {                                                                             \
-                    v[u * RP + r].x = exr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];                    \
-                    v[u * RP + r].y = exi[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];                    \
-                }                                                                                    \
-            }                                                                                        \
-        }                                                                                            \
-        _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
-        {                                                                                            \
-            const int j = t + P * u;                                                                 \
-            dit_stages<T, KP, true, TMA_PACK>(v + u * RP, sp, (j & (ns - 1)), tw,              \
-                              (PRE && p > 0) ? &pre[p][u * KP] : nullptr);                       \
-        }                                                                                            \
-        if (p < NPASS - 1) {                                                                         \
-            if (p > 0) __syncthreads();                                                              \
-            _Pragma("unroll") for (int u = 0; u < U; ++u)                                            \
-            {                                                                                        \
-                const int j = t + P * u;                                                             \
-                const int base = (j >> sp) * ns * RP + (j & (ns - 1));                               \
-                _Pragma("unroll") for (int f = 0; f < RP; ++f)                                       \
-                {                                                                                    \
-                    const int e = base + ns * f;                                                     \
-                    exr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, (t >> sp) * ns * RP + (t & (ns - 1)), ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f)] = v[u * RP + brev(f, KP)].x;              \
-                    exi[ex_wr<T, LOGN, LR, Sh::NT>(p, e, (t >> sp) * ns * RP + (t & (ns - 1)), ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f)] = v[u * RP + brev(f, KP)].y;              \
-                }                                                                                    \
-            }                                                                                        \
-            if (p == 0) {                                                                            \
-                /* input stage consumed; output buffer `ob` must be free before B1 */              \
-                if (tid == 0) bulk_wait_read<OB - 1>();                                             \
-                __syncthreads();                                                                     \
-                if (tid == 0 && k + STAGES < nk) issue_load(st, tile + (int64_t)STAGES * gridDim.x); \
-            } else {                                                                                 \
-                __syncthreads();                                                                     \
-            }                                                                                        \
-        } else {                                                                                     \
-            if (NPASS == 1) {                                                                        \
-                if (tid == 0) bulk_wait_read<OB - 1>();                                             \
-                __syncthreads();                                                                     \
-                if (tid == 0 && k + STAGES < nk) issue_load(st, tile + (int64_t)STAGES * gridDim.x); \
-            }                                                                                        \
-            _Pragma("unroll") for (int u = 0; u < U; ++u)                                            \
-            {                                                                                        \
-                const int j = t + P * u;                                                             \
-                _Pragma("unroll") for (int f = 0; f < RP; ++f)                                       \
-                {                                                                                    \
-                    const int e = j + ns * f;                                                        \
-                    T re = v[u * RP + brev(f, KP)].x, im = v[u * RP + brev(f, KP)].y;                  \
-                    if (do_scale) { re *= scale; im *= scale; }                                      \
-                    sts_at<T>(outr, swz<T, N>(sl, e), re);                                           \
-                    sts_at<T>(outi, swz<T, N>(sl, e), im);                                           \
-                }                                                                                    \
-            }                                                                                        \
-        }                                                                                            \
-    }
-                SFFT_TMA_DIT(1)
-                SFFT_TMA_DIT(2)
-                SFFT_TMA_DIT(3)
-                SFFT_TMA_DIT(4)
-                SFFT_TMA_DIT(5)
-#undef SFFT_TMA_DIT
-            }
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int r = 0; r < RP; ++r) {
+                            const int e = t + P * u + r * (N / RP);
+                            v[u * RP + r].x = lds_at<T>(inr, swz<T, N>(sl, e));
+                            v[u * RP + r].y = lds_at<T>(ini, swz<T, N>(sl, e));
+                        }
+                } else if constexpr (LAST && PX) {
+                    with_g<0, RP>(g, [&](auto GC) {
+                        constexpr int G = decltype(GC)::value;
+                        vec2_t<T> own[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) own[u] = v[brev(G + RP * u, LR)];
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int r = 0; r < RP; ++r) {
+                                const int e = t + P * u + r * (N / RP);
+                                if (r == G) {
+                                    v[u * RP + r] = own[u];
+                                } else {
+                                    const int x = ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP));
+                                    v[u * RP + r].x = exr[x];
+                                    v[u * RP + r].y = exi[x];
+                                }
+                            }
+                    });
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int r = 0; r < RP; ++r) {
+                            const int e = t + P * u + r * (N / RP);
+                            const int x = ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP));
+                            v[u * RP + r].x = exr[x];
+                            v[u * RP + r].y = exi[x];
+                        }
+                }
+                // stages sp+1 .. sp+KP
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = t + P * u;
+                    dit_stages<T, KP, true, TMA_PACK>(v + u * RP, sp, (j & (ns - 1)), tw,
+                                                      (PRE && p > 0) ? &pre[p][u * KP] : nullptr,
+                                                      (HOIST && p > 0) ? hwp(p, u, RP) : nullptr);
+                }
+                if constexpr (!LAST) {
+                    // Stockham scatter
+                    if constexpr (!FIRST) __syncthreads();
+                    if constexpr (p == NPASS - 2 && PX) {
+                        static_assert(U == 1, "the pass before the last runs the full radix");
+                        with_g<0, RPL>(g, [&](auto GC) {
+                            constexpr int G = decltype(GC)::value;
+#pragma unroll
+                            for (int f = 0; f < RP; ++f) {
+                                if (f % RPL == G) continue;      // stays in registers
+                                const int x = ex_wr<T, LOGN, LR, Sh::NT>(p, et + ns * f, et, ns * f);
+                                exr[x] = v[brev(f, KP)].x;
+                                exi[x] = v[brev(f, KP)].y;
+                            }
+                        });
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int j = t + P * u;
+                            const int base = (j >> sp) * ns * RP + (j & (ns - 1));
+#pragma unroll
+                            for (int f = 0; f < RP; ++f) {
+                                const int x = ex_wr<T, LOGN, LR, Sh::NT>(
+                                    p, base + ns * f, et, ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f);
+                                exr[x] = v[u * RP + brev(f, KP)].x;
+                                exi[x] = v[u * RP + brev(f, KP)].y;
+                            }
+                        }
+                    }
+                    if constexpr (FIRST) release_input();
+                    else __syncthreads();
+                } else {
+                    if constexpr (NPASS == 1) release_input();
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int f = 0; f < RP; ++f)
+                            put(t + P * u + ns * f, v[u * RP + brev(f, KP)].x, v[u * RP + brev(f, KP)].y);
+                }
+            });
         } else {
-            // ---------------- DIF (transpose) ----------------
+            // ---------------- DIF (transpose): passes NPASS-1 .. 0 ----------------
+            static_for<0, NPASS>([&](auto QC) {
+                constexpr int q = decltype(QC)::value;
+                constexpr int p = NPASS - 1 - q;
+                constexpr int sp = p * LR, KP = cmin(LR, LOGN - sp), RP = 1 << KP, U = R / RP, ns = 1 << sp;
+                constexpr bool FIRST = q == 0, LAST = p == 0;
+                const int et = (t >> sp) * ns * RP + (t & (ns - 1));
+                // gather
+                if constexpr (FIRST) {
 #pragma unroll
-            for (int q = 0; q < NPASS; ++q) {
-                const int p = NPASS - 1 - q;
-                const int sp = p * LR;
-                const int kp = cmin(LR, LOGN - sp);
-#define SFFT_TMA_DIF(KP)                                                                              \
-    if constexpr (KP <= LR) if (kp == KP) {                                                          \
-        constexpr int RP = 1 << KP, U = R / RP;                                                      \
-        const int ns = 1 << sp;                                                                      \
-        _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
-        {                                                                                            \
-            const int j = t + P * u;                                                                 \
-            const int base = (j >> sp) * ns * RP + (j & (ns - 1));                                   \
-            _Pragma("unroll") for (int f = 0; f < RP; ++f)                                           \
-            {                                                                                        \
-                const int e = base + ns * f;                                                         \
-                const int d = u * RP + brev(f, KP);                                                  \
-                if (q == 0) {                                                                        \
-                    v[d].x = lds_at<T>(inr, swz<T, N>(sl, e));                                        \
-                    v[d].y = lds_at<T>(ini, swz<T, N>(sl, e));                                        \
-                } else {                                                                             \
-                    v[d].x = exr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, (t >> sp) * ns * RP + (t & (ns - 1)), ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f)];                                 \
-                    v[d].y = exi[ex_wr<T, LOGN, LR, Sh::NT>(p, e, (t >> sp) * ns * RP + (t & (ns - 1)), ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f)];                                 \
-                }                                                                                    \
-            }                                                                                        \
-        }                                                                                            \
-        _Pragma("unroll") for (int u = 0; u < U; ++u)                                                \
-        {                                                                                            \
-            const int j = t + P * u;                                                                 \
-            dif_stages<T, KP, true, TMA_PACK>(v + u * RP, sp, (j & (ns - 1)), tw,              \
-                              (PRE && p > 0) ? &pre[p][u * KP] : nullptr);                       \
-        }                                                                                            \
-        if (p > 0) {                                                                                 \
-            if (q > 0) __syncthreads();                                                              \
-            _Pragma("unroll") for (int u = 0; u < U; ++u)                                            \
-            {                                                                                        \
-                const int j = t + P * u;                                                             \
-                _Pragma("unroll") for (int r = 0; r < RP; ++r)                                       \
-                {                                                                                    \
-                    const int e = j + r * (N / RP);                                                  \
-                    exr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].x;                    \
-                    exi[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].y;                    \
-                }                                                                                    \
-            }                                                                                        \
-            if (q == 0) {                                                                            \
-                if (tid == 0) bulk_wait_read<OB - 1>();                                             \
-                __syncthreads();                                                                     \
-                if (tid == 0 && k + STAGES < nk) issue_load(st, tile + (int64_t)STAGES * gridDim.x); \
-            } else {                                                                                 \
-                __syncthreads();                                                                     \
-            }                                                                                        \
-        } else {                                                                                     \
-            if (NPASS == 1) {                                                                        \
-                if (tid == 0) bulk_wait_read<OB - 1>();                                             \
-                __syncthreads();                                                                     \
-                if (tid == 0 && k + STAGES < nk) issue_load(st, tile + (int64_t)STAGES * gridDim.x); \
-            }                                                                                        \
-            _Pragma("unroll") for (int u = 0; u < U; ++u)                                            \
-            {                                                                                        \
-                const int j = t + P * u;                                                             \
-                _Pragma("unroll") for (int r = 0; r < RP; ++r)                                       \
-                {                                                                                    \
-                    const int e = j + r * (N / RP);                                                  \
-                    T re = v[u * RP + r].x, im = v[u * RP + r].y;                                      \
-                    if (do_scale) { re *= scale; im *= scale; }                                      \
-                    sts_at<T>(outr, swz<T, N>(sl, e), re);                                           \
-                    sts_at<T>(outi, swz<T, N>(sl, e), im);                                           \
-                }                                                                                    \
-            }                                                                                        \
-        }                                                                                            \
-    }
-                SFFT_TMA_DIF(1)
-                SFFT_TMA_DIF(2)
-                SFFT_TMA_DIF(3)
-                SFFT_TMA_DIF(4)
-                SFFT_TMA_DIF(5)
-#undef SFFT_TMA_DIF
+                    for (int u = 0; u < U; ++u) {
+                        const int j = t + P * u;
+                        const int base = (j >> sp) * ns * RP + (j & (ns - 1));
+#pragma unroll
+                        for (int f = 0; f < RP; ++f) {
+                            const int e = base + ns * f;
+                            const int d = u * RP + brev(f, KP);
+                            v[d].x = lds_at<T>(inr, swz<T, N>(sl, e));
+                            v[d].y = lds_at<T>(ini, swz<T, N>(sl, e));
+                        }
+                    }
+                } else if constexpr (p == NPASS - 2 && PX) {
+                    static_assert(U == 1, "the pass after the first runs the full radix");
+                    with_g<0, RPL>(g, [&](auto GC) {
+                        constexpr int G = decltype(GC)::value;
+                        constexpr int UL = R / RPL;
+                        vec2_t<T> own[UL];
+#pragma unroll
+                        for (int u = 0; u < UL; ++u) own[u] = v[u * RPL + G];
+#pragma unroll
+                        for (int f = 0; f < RP; ++f) {
+                            const int d = brev(f, KP);
+                            if (f % RPL == G) {
+                                v[d] = own[f / RPL];
+                            } else {
+                                const int x = ex_wr<T, LOGN, LR, Sh::NT>(p, et + ns * f, et, ns * f);
+                                v[d].x = exr[x];
+                                v[d].y = exi[x];
+                            }
+                        }
+                    });
+                } else {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int j = t + P * u;
+                        const int base = (j >> sp) * ns * RP + (j & (ns - 1));
+#pragma unroll
+                        for (int f = 0; f < RP; ++f) {
+                            const int d = u * RP + brev(f, KP);
+                            const int x = ex_wr<T, LOGN, LR, Sh::NT>(
+                                p, base + ns * f, et, ((P * u) >> sp) * ns * RP + ((P * u) & (ns - 1)) + ns * f);
+                            v[d].x = exr[x];
+                            v[d].y = exi[x];
+                        }
+                    }
+                }
+                // stages sp+KP .. sp+1
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int j = t + P * u;
+                    dif_stages<T, KP, true, TMA_PACK>(v + u * RP, sp, (j & (ns - 1)), tw,
+                                                      (PRE && p > 0) ? &pre[p][u * KP] : nullptr,
+                                                      (HOIST && p > 0) ? hwp(p, u, RP) : nullptr);
+                }
+                if constexpr (!LAST) {
+                    if constexpr (!FIRST) __syncthreads();
+                    if constexpr (FIRST && PX) {
+                        with_g<0, RP>(g, [&](auto GC) {
+                            constexpr int G = decltype(GC)::value;
+#pragma unroll
+                            for (int u = 0; u < U; ++u)
+#pragma unroll
+                                for (int r = 0; r < RP; ++r) {
+                                    if (r == G) continue;        // stays in registers
+                                    const int e = t + P * u + r * (N / RP);
+                                    const int x = ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP));
+                                    exr[x] = v[u * RP + r].x;
+                                    exi[x] = v[u * RP + r].y;
+                                }
+                        });
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int r = 0; r < RP; ++r) {
+                                const int e = t + P * u + r * (N / RP);
+                                const int x = ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP));
+                                exr[x] = v[u * RP + r].x;
+                                exi[x] = v[u * RP + r].y;
+                            }
+                    }
+                    if constexpr (FIRST) release_input();
+                    else __syncthreads();
+                } else {
+                    if constexpr (NPASS == 1) release_input();
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+#pragma unroll
+                        for (int r = 0; r < RP; ++r)
+                            put(t + P * u + r * (N / RP), v[u * RP + r].x, v[u * RP + r].y);
+                }
+            });
+        }
+        if constexpr (OB == 0) {
+            // the next tile's first scatter reuses the exchange buffer
+            if constexpr (NPASS >= 2) __syncthreads();
+        } else {
+            // output tile complete in shared memory -> one TMA store per plane
+            fence_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+                const int row0 = (int)(tile * S);
+                tma_store_3d(&out_re, outr, 0, 0, row0);
+                tma_store_3d(&out_im, outi, 0, 0, row0);
+                bulk_commit();
             }
         }
-        // output tile complete in shared memory -> one TMA store per plane
-        fence_async_smem();
-        __syncthreads();
-        if (tid == 0) {
-            const int row0 = (int)(tile * S);
-            tma_store_3d(&out_re, outr, 0, 0, row0);
-            tma_store_3d(&out_im, outi, 0, 0, row0);
-            bulk_commit();
-        }
     }
-    if (tid == 0) bulk_wait_all();
+    if (OB > 0 && tid == 0) bulk_wait_all();
     (void)W;
+}
+
+// MINB = 0: no min-blocks hint (an explicit 1 is not the default: the cfg2
+// shape went from 48 to 71 registers with it); MINB > 0 caps the registers
+// so MINB CTAs fit an SM (fp64 N = 1024: 4 x 128 threads at <= 128).
+template <typename T, int LOGN, int LR_REQ, bool DIF, int NT_REQ, int STAGES, int OB, bool PRE_T = false,
+          int MINB = 0>
+__global__ void __launch_bounds__(TmaShape<T, LOGN, LR_REQ, NT_REQ, STAGES, OB>::NT)
+sfft_tma_kernel(const __grid_constant__ CUtensorMap in_re, const __grid_constant__ CUtensorMap in_im,
+                const __grid_constant__ CUtensorMap out_re, const __grid_constant__ CUtensorMap out_im,
+                const TmaArgs a)
+{
+    tma_body<T, LOGN, LR_REQ, DIF, NT_REQ, STAGES, OB, PRE_T>(in_re, in_im, out_re, out_im, a);
+}
+
+template <typename T, int LOGN, int LR_REQ, bool DIF, int NT_REQ, int STAGES, int OB, bool PRE_T, int MINB>
+__global__ void __launch_bounds__(TmaShape<T, LOGN, LR_REQ, NT_REQ, STAGES, OB>::NT, MINB)
+sfft_tma_kernel_mb(const __grid_constant__ CUtensorMap in_re, const __grid_constant__ CUtensorMap in_im,
+                   const __grid_constant__ CUtensorMap out_re, const __grid_constant__ CUtensorMap out_im,
+                   const TmaArgs a)
+{
+    tma_body<T, LOGN, LR_REQ, DIF, NT_REQ, STAGES, OB, PRE_T>(in_re, in_im, out_re, out_im, a);
+}
+
+template <typename T, int LOGN, int LR_REQ, bool DIF, int NT_REQ, int STAGES, int OB, bool PRE_T, int MINB>
+constexpr auto tma_kernel_for()
+{
+    if constexpr (MINB > 0) return &sfft_tma_kernel_mb<T, LOGN, LR_REQ, DIF, NT_REQ, STAGES, OB, PRE_T, MINB>;
+    else return &sfft_tma_kernel<T, LOGN, LR_REQ, DIF, NT_REQ, STAGES, OB, PRE_T, 0>;
 }
 
 }  // namespace sfft

@@ -42,29 +42,41 @@ inline cudaError_t encode_plane(CUtensorMap *map, const void *ptr, int n, int64_
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <typename T, int LOGN, int LR, bool DIF, int NT_REQ, int STAGES, int OB, bool PRE>
+// Resident CTAs of kernel `k` on device `dev` (shared-memory attribute set
+// once per device and kernel).  Initialised under std::call_once per device,
+// so concurrent first calls never see a half-written entry.
+struct Residency {
+    std::once_flag once[64];
+    cudaError_t err[64] = {};
+    int grid[64] = {};
+    template <typename K>
+    cudaError_t get(K k, int dev, int nt, int smem, int *out)
+    {
+        if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+        std::call_once(once[dev], [&] {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            int b = 0, sms = 0;
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, nt, smem);
+            if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (e == cudaSuccess && b < 1) e = cudaErrorInvalidConfiguration;
+            err[dev] = e;
+            grid[dev] = e == cudaSuccess ? b * sms : 0;
+        });
+        *out = grid[dev];
+        return err[dev];
+    }
+};
+
+template <typename T, int LOGN, int LR, bool DIF, int NT_REQ, int STAGES, int OB, bool PRE, int MINB = 0>
 cudaError_t launch_tma(const TmaLaunch &L, cudaStream_t st)
 {
     using Sh = TmaShape<T, LOGN, LR, NT_REQ, STAGES, OB>;
-    auto k = sfft_tma_kernel<T, LOGN, LR, DIF, NT_REQ, STAGES, OB, PRE>;
-    static int blocks_per_sm[32] = {0};
-    static int num_sms[32] = {0};
-    int dev = 0;
+    auto k = tma_kernel_for<T, LOGN, LR, DIF, NT_REQ, STAGES, OB, PRE, MINB>();
+    static Residency res;
+    int dev = 0, resident = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    dev &= 31;
-    if (!blocks_per_sm[dev]) {
-        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Sh::SMEM);
-        if (e != cudaSuccess) return e;
-        int b = 0, sms = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k, Sh::NT, Sh::SMEM);
-        if (e != cudaSuccess) return e;
-        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (e != cudaSuccess) return e;
-        if (b < 1) return cudaErrorInvalidConfiguration;
-        num_sms[dev] = sms;
-        blocks_per_sm[dev] = b;
-    }
+    if ((e = res.get(k, dev, Sh::NT, Sh::SMEM, &resident)) != cudaSuccess) return e;
     // the caller realises the inverse by swapping the re/im maps (channel swap)
     const void *xr = L.inverse ? L.x_im : L.x_re;
     const void *xi = L.inverse ? L.x_re : L.x_im;
@@ -74,16 +86,25 @@ cudaError_t launch_tma(const TmaLaunch &L, cudaStream_t st)
     constexpr int N = Sh::N;
     if ((e = encode_plane<T>(&m_xr, xr, N, L.batch, L.in_stride, Sh::S)) != cudaSuccess) return e;
     if ((e = encode_plane<T>(&m_xi, xi, N, L.batch, L.in_stride, Sh::S)) != cudaSuccess) return e;
-    if ((e = encode_plane<T>(&m_yr, yr, N, L.batch, L.out_stride, Sh::S)) != cudaSuccess) return e;
-    if ((e = encode_plane<T>(&m_yi, yi, N, L.batch, L.out_stride, Sh::S)) != cudaSuccess) return e;
+    if constexpr (OB > 0) {
+        if ((e = encode_plane<T>(&m_yr, yr, N, L.batch, L.out_stride, Sh::S)) != cudaSuccess) return e;
+        if ((e = encode_plane<T>(&m_yi, yi, N, L.batch, L.out_stride, Sh::S)) != cudaSuccess) return e;
+    } else {
+        m_yr = m_xr;   // unused: the last pass stores directly (a.y_re / a.y_im)
+        m_yi = m_xi;
+    }
     TmaArgs a;
     a.ntiles = (L.batch + Sh::S - 1) / Sh::S;
     a.scale = L.scale;
     a.scale_out = L.inverse;
     a.tw = L.tw;
-    int64_t grid = (int64_t)num_sms[dev] * blocks_per_sm[dev];
+    a.y_re = yr;
+    a.y_im = yi;
+    a.batch = L.batch;
+    a.out_stride = L.out_stride;
+    int64_t grid = resident;
     if (grid > a.ntiles) grid = a.ntiles;
-    if (grid < 1) grid = 1;
+    if (grid < 1) return cudaErrorInvalidConfiguration;   // batch > 0 here: never silently skip work
 #ifndef SFFT_TMA_NO_PDL
     // programmatic dependent launch: this grid may be scheduled while the
     // previous kernel of the stream drains; the kernel's griddepcontrol.wait

@@ -34,12 +34,35 @@ exchange, gather) is testable on CPU with gloo (tests/test_dist_gloo.py).
 """
 
 import ctypes
+import datetime
+import os
 
 import numpy as np
 import torch
 
 from . import _ffi
 from .transform import _DTYPE_CODE, _resolve_device, _stream_ptr
+
+
+DEFAULT_TIMEOUT_S = 300
+
+
+def init_process_group(backend: str = "nccl", device=None, timeout_s: float = DEFAULT_TIMEOUT_S):
+    """torch.distributed setup with the failure handling this library relies
+    on: a bounded collective timeout (a hung peer raises instead of blocking
+    forever), NCCL asynchronous error handling (a failed communicator aborts
+    the process rather than leaving it spinning), and NCCL INIT logs on
+    stderr so a launcher can confirm the communicator size."""
+    import torch.distributed as dist
+    os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
+    if backend == "nccl":
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+    kw = {"timeout": datetime.timedelta(seconds=timeout_s)}
+    if backend == "nccl" and device is not None:
+        kw["device_id"] = torch.device(device)
+    dist.init_process_group(backend, **kw)
 
 
 def shard_rows(batch: int, world: int, rank: int):
@@ -76,6 +99,11 @@ class DistPlan:
         ws = ctypes.c_size_t()
         _ffi.check(_ffi.lib.sfft_dist_workspace_bytes(self._handle, ctypes.byref(ws)))
         self.workspace_bytes = ws.value
+        l0, l1_ = ctypes.c_int(), ctypes.c_int()
+        _ffi.check(_ffi.lib.sfft_dist_schedule(self._handle, ctypes.byref(l0), ctypes.byref(l1_)))
+        # pass-kernel launches of phase 0 / phase 1; each reads and writes the
+        # rank's N/G elements of both planes once (the HBM sweeps of a step)
+        self.launches = (l0.value, l1_.value)
 
     def __del__(self):
         h = getattr(self, "_handle", None)

@@ -113,7 +113,7 @@ class FftPlan:
     def kernel(self) -> str:
         """Kernel family used for aligned planar rows: 'tma', 'ldg' or 'pass'."""
         return {_ffi.SFFT_KERNEL_TMA: "tma", _ffi.SFFT_KERNEL_LDG: "ldg",
-                _ffi.SFFT_KERNEL_PASS: "pass", _ffi.SFFT_KERNEL_PAIR: "pair"}[self._info()[6]]
+                _ffi.SFFT_KERNEL_PASS: "pass"}[self._info()[6]]
 
     def workspace_bytes(self, batch: int) -> int:
         out = ctypes.c_size_t()
@@ -158,8 +158,7 @@ def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
     the plane dtype (float64 like the reference, or float32); ``radix_log``
     overrides the register radix of the fused kernel (0 = tuned default);
     ``kernel`` picks the fused kernel family: "auto" (TMA-fed when the rows
-    allow it), "ldg" (per-thread loads), "tma" (required) or "pair" (fp32
-    planar, two signals per thread packed across the pair; batch >= 2);
+    allow it), "ldg" (per-thread loads) or "tma" (required);
     ``prefetch_factors`` (fp32) forces fetching each pass's base factors
     before the data on/off (None = tuned default).
     """
@@ -171,8 +170,7 @@ def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
     if dtype not in _DTYPE_CODE:
         raise ValueError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
     device = _resolve_device(device)
-    kernels = {"auto": _ffi.SFFT_KERNEL_AUTO, "ldg": _ffi.SFFT_KERNEL_LDG, "tma": _ffi.SFFT_KERNEL_TMA,
-               "pair": _ffi.SFFT_KERNEL_PAIR}
+    kernels = {"auto": _ffi.SFFT_KERNEL_AUTO, "ldg": _ffi.SFFT_KERNEL_LDG, "tma": _ffi.SFFT_KERNEL_TMA}
     if kernel not in kernels:
         raise ValueError(f"kernel must be one of {sorted(kernels)}, got {kernel!r}")
     kcode = kernels[kernel] | {None: 0, False: 0x10, True: 0x20}[prefetch_factors]

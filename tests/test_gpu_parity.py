@@ -94,45 +94,6 @@ def test_every_radix_schedule(cuda, m, lr, algo, dtype, prefetch):
         assert rel_l2(gr.astype(np.float64), gi.astype(np.float64), wr, wi) <= F32_TOL(m)
 
 
-@pytest.mark.parametrize("inverse", [False, True])
-@pytest.mark.parametrize("algo", ["dit", "dif"])
-@pytest.mark.parametrize("m,lr,b", [(m, lr, b) for m in (4, 6, 8, 10, 11, 12) for lr in (2, 3, 4)
-                                    if (1 << (m - min(lr, m))) <= 1024 for b in (2, 7)])
-def test_pair_kernel(cuda, m, lr, b, algo, inverse):
-    """fp32 two-signals-per-thread kernel: the single-signal kernel's values
-    (same per-lane rounding) and the oracle tolerance; odd batches pad the
-    last pair."""
-    rng = np.random.default_rng(5000 + 16 * m + lr + b)
-    re, im = rand(rng, b, 1 << m, np.float32)
-    plan = sf.make_plan(m, algo, dtype=torch.float32, device="cuda:0", radix_log=lr, kernel="pair")
-    assert plan.kernel == "pair"
-    yr, yi = sf.fft_split(torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda(), inverse=inverse, plan=plan)
-    gr, gi = yr.cpu().numpy(), yi.cpu().numpy()
-    ldg = sf.make_plan(m, algo, dtype=torch.float32, device="cuda:0", radix_log=lr, kernel="ldg",
-                       prefetch_factors=False)
-    lr_, li_ = sf.fft_split(torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda(), inverse=inverse, plan=ldg)
-    assert np.array_equal(gr.view(np.int32), lr_.cpu().numpy().view(np.int32))
-    assert np.array_equal(gi.view(np.int32), li_.cpu().numpy().view(np.int32))
-    wr, wi = oracle.fft_split_c(re, im, algo, inverse)
-    assert rel_l2(gr.astype(np.float64), gi.astype(np.float64), wr, wi) <= F32_TOL(m)
-
-
-@pytest.mark.parametrize("stride_pad", [0, 5])
-def test_pair_kernel_strides_and_single_row(cuda, stride_pad):
-    """Row strides other than N, and batch 1 (which takes the LDG kernel)."""
-    m = 10
-    n = 1 << m
-    rng = np.random.default_rng(77 + stride_pad)
-    big_r = torch.from_numpy(rng.standard_normal((5, n + stride_pad)).astype(np.float32)).cuda()
-    big_i = torch.from_numpy(rng.standard_normal((5, n + stride_pad)).astype(np.float32)).cuda()
-    xr, xi = big_r[:, :n], big_i[:, :n]
-    plan = sf.make_plan(m, "dit", dtype=torch.float32, device="cuda:0", radix_log=4, kernel="pair")
-    for rows in (5, 1):
-        yr, yi = sf.fft_split(xr[:rows], xi[:rows], plan=plan)
-        wr, wi = oracle.fft_split_c(xr[:rows].cpu().numpy(), xi[:rows].cpu().numpy(), "dit", False)
-        assert rel_l2(yr.cpu().numpy().astype(np.float64), yi.cpu().numpy().astype(np.float64), wr, wi) <= F32_TOL(m)
-
-
 @pytest.mark.parametrize("m", [3, 6, 10, 12, 14])
 @pytest.mark.parametrize("algo", ["dit", "dif"])
 def test_interleaved_in_place_matches_split(cuda, m, algo):
@@ -303,8 +264,7 @@ def test_host_pipeline_many_chunks(cuda, monkeypatch, pinned):
         assert torch.equal(out_r, dr.cpu()) and torch.equal(out_i, di.cpu())
 
 
-PASS_VARIANTS = {"tma": {"SFFT_PASS_TMA": "1"}, "async": {"SFFT_PASS_ASYNC": "1"},
-                 "plain": {"SFFT_PASS_ASYNC": "0"}}
+PASS_VARIANTS = {"plain": {}, "split_8_5": {"SFFT_PASS_SPLIT": "8,5"}}
 
 
 @pytest.mark.parametrize("variant", sorted(PASS_VARIANTS))
@@ -312,9 +272,8 @@ PASS_VARIANTS = {"tma": {"SFFT_PASS_TMA": "1"}, "async": {"SFFT_PASS_ASYNC": "1"
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
 @pytest.mark.parametrize("m", [13, 16, 20])
 def test_pass_kernel_variants(cuda, m, dtype, algo, variant):
-    # each pass-kernel family for the groups with S > 0, forced through its
-    # environment switch in a subprocess: the TMA-pipelined kernel (opt-in),
-    # the persistent cp.async kernel and the plain LDG pass kernel
+    # the pass schedule in a subprocess: default group split, and (m = 13
+    # only) an unbalanced split through the developer knob
     import subprocess
     import sys
     code = f"""
@@ -365,48 +324,3 @@ def test_cuda_graph_capture_and_replay(cuda, m):
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(yr, want[0]) and torch.equal(yi, want[1])
-
-
-@pytest.mark.parametrize("discard", ["1", "0"])
-@pytest.mark.parametrize("m,block_log", [(18, 12), (20, 13), (22, 14), (23, 21)])
-def test_l2_blocked_schedule_f64_bitwise(cuda, monkeypatch, m, block_log, discard):
-    # the L2-blocked long-transform schedule (sfft_abi.cu exec_blocked),
-    # forced at small sizes with small blocks: still bitwise the reference's
-    # fp64 results, forward and inverse, with and without the L2 discards
-    monkeypatch.setenv("SFFT_BLOCKED", "1")
-    monkeypatch.setenv("SFFT_BLOCK_MIN_M", "13")
-    monkeypatch.setenv("SFFT_BLOCK_LOG", str(block_log))
-    monkeypatch.setenv("SFFT_L2_DISCARD", discard)
-    plan = sf.make_plan(m, dtype=torch.float64, device="cuda:0")
-    nl, ns = plan.schedule(1)
-    assert ns == 2 and nl > 4
-    assert plan.schedule(2) == (plan.launches_per_exec, plan.launches_per_exec)   # batch > 1: unblocked
-    rng = np.random.default_rng(m)
-    re = rng.standard_normal((1, 1 << m))
-    im = rng.standard_normal((1, 1 << m))
-    for inv in (False, True):
-        yr, yi = sf.fft_split(torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda(), plan=plan, inverse=inv)
-        wr, wi = oracle.fft_split_c(re, im, "dit", inv)
-        assert np.array_equal(bits(yr.cpu().numpy()), bits(wr)) and np.array_equal(bits(yi.cpu().numpy()), bits(wi))
-
-
-@pytest.mark.parametrize("m", [23, 24])
-def test_l2_blocked_schedule_f32(cuda, monkeypatch, m):
-    # fp32 at its intended sizes: against the oracle and the 4-sweep schedule
-    plan = sf.make_plan(m, dtype=torch.float32, device="cuda:0")
-    rng = np.random.default_rng(m + 1)
-    re = rng.standard_normal((1, 1 << m)).astype(np.float32)
-    im = rng.standard_normal((1, 1 << m)).astype(np.float32)
-    xr, xi = torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda()
-    ur, ui = sf.fft_split(xr, xi, plan=plan)
-    assert plan.schedule(1)[1] == plan.launches_per_exec
-    monkeypatch.setenv("SFFT_BLOCKED", "1")
-    assert plan.schedule(1)[1] == 2
-    yr, yi = sf.fft_split(xr, xi, plan=plan)
-    wr, wi = oracle.fft_split_c(re, im)
-    gr, gi = yr.cpu().numpy().astype(np.float64), yi.cpu().numpy().astype(np.float64)
-    err = np.sqrt(np.sum((gr - wr) ** 2 + (gi - wi) ** 2) / np.sum(wr ** 2 + wi ** 2))
-    assert err <= 1e-5 * m
-    num = torch.sqrt(torch.sum((yr - ur).double() ** 2 + (yi - ui).double() ** 2))
-    den = torch.sqrt(torch.sum(ur.double() ** 2 + ui.double() ** 2))
-    assert (num / den).item() <= 1e-6

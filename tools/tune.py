@@ -62,8 +62,6 @@ def main():
             if dt == "f32":   # both settings of the up-front base factors
                 variants = [(k, lr, pf) for k, lr, _ in variants for pf in (False, True)
                             if not (pf and (lr < 2 or m < 5))]
-                # two signals per thread (no up-front factor option)
-                variants += [("pair", lr, None) for lr in (2, 3, 4) if lr <= m and (n >> lr) <= 1024]
             best = None
             for kern, lr, pf in variants:
                 try:
