@@ -4,17 +4,26 @@
 
 A step is one pass of the hot path -- one batched forward transform of the
 whole config batch (one kernel launch for N <= 4096) -- over inputs already
-resident in HBM.  Default workload: BASELINE.json configs[1] (N=64 fp32,
-B=2^20, seed 1, standard normal).  Under torchrun each rank transforms its
-own B-row batch on its own GPU (weak scaling, no collective on the data
-path); the timed region is bracketed by barrier + synchronize, timed with
-CUDA events on the launching stream, and the max over ranks is reported.
+resident in HBM.  Default workload: BASELINE.json configs[2] in its fp64
+variant (N=1024, B=2^18, seed 2, uniform[-1,1)) -- the largest single-GPU
+configuration and the reference's own arithmetic (fp64 only,
+layout.py:29-30); the other configs via --config.  With N GPUs
+(``--gpus N``: spawned here with torchrun when WORLD_SIZE is unset) the
+batch is split into N contiguous row blocks (``--scaling strong``, the
+default, BASELINE configs[2] / SURVEY 8e) or every rank transforms its own
+B rows (``--scaling weak``); no collective on the data path.  Config 5 (one
+N = 2^28 transform) runs the sharded four-step.  The timed region is
+bracketed by barrier + synchronize, timed with CUDA events on the launching
+stream, and the max over ranks is reported.
 
 Rank 0 prints ONE JSON line with the driver contract keys plus
 ``roofline`` (HBM-bound: algorithmic bytes 4*N*sizeof(real) per transform /
 the measured kernel duration, against MEASURED_PEAKS.json hbm_gbs),
 ``cpu_baseline`` (the oracle's numpy restatement of the reference executor,
-timed on this host's cores on a bounded sample of the same workload),
+timed on this host's cores on a bounded sample of the same workload, plus
+its one-process rate) and ``parity`` (relative L2 / bitwise agreement of
+sampled rows of the timed output with the C oracle -- the checker, run
+after the timed region),
 ``e2e`` (the same metric through the public ``fft_split`` on pinned HOST
 buffers, H2D + D2H inside the timed region), ``gpu_launches`` and
 ``clocks`` (NVML samples taken during the timed region).
@@ -25,8 +34,11 @@ config and prints the same line with ``"impl": "reference"``.
 """
 
 import argparse
+import hashlib
 import json
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -48,7 +60,12 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2_n64_f32", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--config", default="cfg3_n1024_f64", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1 GPUs, batch configs: split the config's B rows across the ranks (strong) "
+                         "or give every rank B rows (weak)")
+    ap.add_argument("--parity-rows", type=int, default=64,
+                    help="rows of the timed output checked against the C oracle after the timed region")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--algorithm", default="dit", choices=["dit", "dif"])
     ap.add_argument("--radix-log", type=int, default=0)
@@ -79,15 +96,39 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(cfg_name):
-    """dram bytes per launch from the committed ncu --set full capture, if any."""
+KERNEL_SRC_DIR = os.path.join(ROOT, "paper_2504_07264_b200", "csrc")
+
+
+def src_hash():
+    """Hash of the kernel sources (hand-written .cu/.cuh/.h and the
+    instantiation generator; the generated units follow from them)."""
+    h = hashlib.sha256()
+    for name in sorted(os.listdir(KERNEL_SRC_DIR)):
+        if name.startswith("sfft_inst_") or name == "sfft_small_tw.h":
+            continue
+        if name.endswith((".cu", ".cuh", ".h", ".py")) or name == "Makefile":
+            with open(os.path.join(KERNEL_SRC_DIR, name), "rb") as f:
+                h.update(name.encode() + b"\0" + f.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_traffic(cfg_name, algorithm="dit"):
+    """(dram bytes per launch, note) from the committed ncu --set full capture
+    of this config -- None unless the capture was taken from the kernel
+    sources this run is built from (same src_hash) with the same algorithm."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(path):
-        return None
+        return None, "no committed ncu capture"
     with open(path) as f:
         d = json.load(f)
     v = d.get(cfg_name)
-    return None if v is None else float(v["dram_bytes_per_launch"])
+    if v is None:
+        return None, "no committed ncu capture for this config"
+    if v.get("src_hash") != src_hash():
+        return None, f"stale: capture {v.get('source')} is of kernel sources {v.get('src_hash')}, not {src_hash()}"
+    if v.get("algorithm", "dit") != algorithm:
+        return None, f"capture is of the {v.get('algorithm', 'dit')} schedule"
+    return float(v["dram_bytes_per_launch"]), f"{v.get('source')} (kernel sources {v.get('src_hash')})"
 
 
 # ---------------------------------------------------------------- clocks ---
@@ -289,6 +330,42 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ ours ---
+def parity_check(cfg, algorithm, xr, xi, yr, yi, row0, rows):
+    """The checker (after the timed region): sampled rows of the timed
+    output against the C oracle (a bit-exact restatement of the reference
+    executor, transform.py:123-270, pinned to reference-generated vectors)
+    on the same inputs.  fp64: bitwise; fp32: relative L2 against the fp64
+    oracle on the same fp32 inputs (north_star: <= 1e-5 * log2 N)."""
+    from oracle import oracle
+    b = xr.shape[0]
+    idx = np.unique(np.linspace(0, b - 1, num=min(rows, b)).astype(np.int64))
+    import torch
+    ti = torch.from_numpy(idx).to(xr.device)
+    xr_s, xi_s = xr.index_select(0, ti).cpu().numpy(), xi.index_select(0, ti).cpu().numpy()
+    gr, gi = yr.index_select(0, ti).cpu().numpy(), yi.index_select(0, ti).cpu().numpy()
+    t0 = time.perf_counter()
+    wr, wi = oracle.fft_split_c(xr_s.astype(np.float64), xi_s.astype(np.float64), algorithm, False)
+    t_oracle = time.perf_counter() - t0
+    d = (gr.astype(np.float64) - wr) ** 2 + (gi.astype(np.float64) - wi) ** 2
+    ref = wr ** 2 + wi ** 2
+    per_row = np.sqrt(d.sum(1) / np.maximum(ref.sum(1), 1e-300))
+    out = {"rows_checked": int(len(idx)), "row_indices": f"{len(idx)} rows evenly spaced over rows "
+           f"[{row0}, {row0 + b}) of the {cfg.name} stream",
+           "oracle": "oracle/liboracle.so (C restatement of transform.py:123-270, bitwise the reference)",
+           "rel_l2_global": float(np.sqrt(d.sum() / ref.sum())), "rel_l2_max_row": float(per_row.max()),
+           "oracle_s": t_oracle}
+    if cfg.dtype == "f64":
+        out["bitwise"] = bool(np.array_equal(gr.view(np.int64), wr.view(np.int64)) and
+                              np.array_equal(gi.view(np.int64), wi.view(np.int64)))
+        out["tolerance"] = "1e-12 (north_star, fp64); bitwise expected"
+        out["pass"] = out["bitwise"] or out["rel_l2_max_row"] <= 1e-12
+    else:
+        tol = 1e-5 * cfg.log2n
+        out["tolerance"] = f"{tol:g} (north_star 1e-5*log2N, fp32)"
+        out["pass"] = out["rel_l2_max_row"] <= tol
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -300,24 +377,28 @@ def run_ours(args):
     local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+        from paper_2504_07264_b200 import dist as sdist
+        sdist.init_process_group(backend, device=torch.device("cuda", local) if backend == "nccl" else None)
     device = torch.device("cuda", local if world > 1 else torch.cuda.current_device())
     torch.cuda.set_device(device)
 
     import paper_2504_07264_b200 as sf
     from paper_2504_07264_b200 import _ffi
+    from paper_2504_07264_b200.dist import shard_rows
 
     cfg = workloads.CONFIGS[args.config]
     dt = torch.float32 if cfg.dtype == "f32" else torch.float64
-    # this rank's batch: rank 0 = the config's canonical stream; others a
-    # seeded variant of the same distribution (weak scaling: B rows per GPU)
-    if rank == 0:
-        re, im = workloads.generate(cfg)
+    # this rank's rows.  strong: rows [r0, r1) of the config's canonical
+    # stream (the B rows split into `world` contiguous blocks); weak: B rows
+    # per rank -- rank 0 the canonical stream, others a seeded variant of
+    # the same distribution
+    if args.scaling == "strong" or world == 1:
+        r0, r1 = shard_rows(cfg.batch, world, rank)
+        re, im = workloads.generate(cfg, rows=r1 - r0, start=r0)
     else:
-        c2 = workloads.Config(cfg.name, cfg.log2n, cfg.batch, cfg.dtype, cfg.seed * 1000 + rank, cfg.dist)
+        r0, r1 = 0, cfg.batch
+        c2 = cfg if rank == 0 else workloads.Config(cfg.name, cfg.log2n, cfg.batch, cfg.dtype,
+                                                    cfg.seed * 1000 + rank, cfg.dist)
         re, im = workloads.generate(c2)
     x_re = torch.from_numpy(re).to(device)
     x_im = torch.from_numpy(im).to(device)
@@ -326,10 +407,10 @@ def run_ours(args):
     y_im = torch.empty_like(x_im)
     plan = sf.make_plan(cfg.log2n, args.algorithm, dtype=dt, device=device, radix_log=args.radix_log)
     stream = torch.cuda.current_stream(device)
-    ws_bytes = plan.workspace_bytes(cfg.batch)
+    b, n = x_re.shape[0], cfg.n
+    ws_bytes = plan.workspace_bytes(b)
     ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=device)
     sp = stream.cuda_stream
-    b, n = cfg.batch, cfg.n
 
     def step():
         _ffi.check(_ffi.lib.sfft_exec_split(plan._handle, x_re.data_ptr(), x_im.data_ptr(),
@@ -339,7 +420,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(device)
-    # the W warm-up steps of a 0.2 ms step leave an idle GPU at low clocks;
+    # the W warm-up steps of a short step leave an idle GPU at low clocks;
     # keep stepping (untimed) until the clocks have ramped (>= SPINUP_S)
     spin0 = time.perf_counter()
     while time.perf_counter() - spin0 < SPINUP_S:
@@ -379,8 +460,7 @@ def run_ours(args):
                 else [total_ms / args.steps] * args.steps)
     ms_local = total_ms / args.steps
     # roofline unit: one HBM sweep (a launch that reads and writes the whole
-    # batch once; the L2-blocked long-transform schedule does 2 sweeps in
-    # many block launches, sfft_exec_schedule)
+    # batch once); N > 4096 runs one launch per stage group
     n_launch, n_sweep = plan.schedule(b)
     kern_local = float(np.mean(per_step)) / n_sweep
 
@@ -391,9 +471,17 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def sum_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=device if backend == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
     ms = max_over_ranks(ms_local)
     kern_ms = max_over_ranks(kern_local)
-    value = world * b / (ms / 1e3)
+    total_rows = int(sum_over_ranks(b))
+    value = total_rows / (ms / 1e3)
 
     # ---------------- e2e through the public API with pinned host buffers
     e2e = None
@@ -417,7 +505,7 @@ def run_ours(args):
         torch.cuda.synchronize(device)
         e2e_ms = max_over_ranks(e0.elapsed_time(e1) / args.e2e_steps)
         ok = torch.equal(ho_r.to(device), y_re) and torch.equal(ho_i.to(device), y_im)
-        e2e = {"value": world * b / (e2e_ms / 1e3), "unit": "transforms/s",
+        e2e = {"value": total_rows / (e2e_ms / 1e3), "unit": "transforms/s",
                "h2d_bytes_per_step": int(hr.numel() * hr.element_size() * 2),
                "d2h_bytes_per_step": int(ho_r.numel() * ho_r.element_size() * 2),
                "ms_per_step": e2e_ms, "api": "paper_2504_07264_b200.fft_split(host pinned re, im, out=host)",
@@ -433,12 +521,13 @@ def run_ours(args):
     peak, peak_src = peaks()
     import dataclasses
     census = dataclasses.asdict(sf.count_flops(cfg.log2n))
-    # every launch reads and writes both planes of the whole batch once: the
+    # every launch reads and writes both planes of the rank's rows once: the
     # fused kernel is the whole transform, each pass-group launch of the
     # multi-launch schedule (N > 4096) moves the same 4*N*sizeof(real) bytes
     bytes_per_launch = 4 * n * cfg.elem_bytes * b
     achieved = bytes_per_launch / (kern_ms / 1e3) / 1e9
-    traffic = ncu_traffic(cfg.name)
+    traffic, traffic_src = ncu_traffic(cfg.name, args.algorithm)
+    kname = {"tma": "sfft_tma_kernel", "ldg": "sfft_fused_kernel", "pass": "sfft_pass_kernel"}[plan.kernel]
     line = {
         "metric": BASELINE_METRIC,
         "value": value,
@@ -448,39 +537,50 @@ def run_ours(args):
         "warmup": args.warmup,
         "ms_per_step": ms,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": args.scaling if world > 1 else "strong",
         "vs_baseline": None,
         "dtype": "f32" if cfg.dtype == "f32" else "f64",
         "data": "synthetic (seeded, BASELINE.json config shapes/distributions; workloads.py)",
-        "config": {"workload": cfg.name, "n": n, "batch_per_gpu": b, "global_batch": b * world,
+        "config": {"workload": cfg.name, "n": n, "batch_per_gpu": b, "global_batch": total_rows,
                    "input_dtype": cfg.dtype, "seed": cfg.seed, "algorithm": args.algorithm,
-                   "radix_log": plan.radix_log, "parallelism": f"batch-sharded x{world}, no collective",
-                   "l2": f"inputs {2 * n * cfg.elem_bytes * b / 2**20:.0f} MiB > 126 MB L2 (no flush needed)",
+                   "radix_log": plan.radix_log,
+                   "parallelism": (f"batch split into {world} contiguous row blocks (strong), no collective"
+                                   if args.scaling == "strong" or world == 1 else
+                                   f"batch-sharded x{world}, B rows per GPU (weak), no collective"),
+                   "l2": f"inputs {2 * n * cfg.elem_bytes * b / 2**20:.0f} MiB per GPU "
+                         f"{'>' if 2 * n * cfg.elem_bytes * b > 126e6 else '<='} 126 MB L2 (no flush)",
                    "extra_warmup_s": SPINUP_S},
-        "gbs_algorithmic": 4 * n * cfg.elem_bytes * b * world / (ms / 1e3) / 1e9,
-        "gflops_5nlogn": 5 * n * cfg.log2n * b * world / (ms / 1e3) / 1e9,
+        "gbs_algorithmic": 4 * n * cfg.elem_bytes * total_rows / (ms / 1e3) / 1e9,
+        "gflops_5nlogn": 5 * n * cfg.log2n * total_rows / (ms / 1e3) / 1e9,
         # the reference's own census (count_flops, transform.py:312-335) next to 5N log2N
         "census": census,
-        "gflops_census": (census["real_mults"] + census["real_adds"]) * b * world / (ms / 1e3) / 1e9,
+        "gflops_census": (census["real_mults"] + census["real_adds"]) * total_rows / (ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "kernel": {"tma": "sfft_tma_kernel", "ldg": "sfft_fused_kernel",
-                                "pass": "sfft_pass_kernel"}[plan.kernel] + f"<{cfg.dtype}, log2N={cfg.log2n}>",
+                     "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                     "kernel": kname + f"<{cfg.dtype}, log2N={cfg.log2n}>",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "unit_of_work": "sweep" if n_launch != n_sweep else "launch",
+                     "unit_of_work": "launch" if n_launch == 1 else "sweep (one pass-group launch)",
                      "sweeps_per_step": n_sweep,
                      "launches_per_step": n_launch,
                      "kernel_ms": kern_ms, "peak_source": peak_src,
-                     "frac_of_datasheet_8tbs": achieved / 8000.0},
+                     "frac_of_datasheet_8tbs": achieved / 8000.0,
+                     "step_frac": bytes_per_launch / (ms / 1e3) / 1e9 / peak,
+                     "kernel_src_hash": src_hash()},
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
     }
     if e2e is not None:
         line["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:
-        rate, procs, sample, _ = cpu_port_rate(cfg, args.algorithm, args.cpu_seconds)
+        # cpu_baseline leg: the reference's CPU path (numpy port) on a
+        # bounded sample, and the checker on sampled rows of the timed output
+        rate, procs, sample, per_row = cpu_port_rate(cfg, args.algorithm, args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "transforms/s", "cores": procs, "kind": "port",
-                                "sample": sample, "cpu_model": cpu_model()}
+                                "sample": sample, "cpu_model": cpu_model(),
+                                "one_process": {"value": 1.0 / per_row, "unit": "transforms/s", "cores": 1,
+                                                "sample": "the sizing probe of the same stream, 1 process"}}
+    if args.parity_rows > 0:
+        line["parity"] = parity_check(cfg, args.algorithm, x_re, x_im, y_re, y_im, r0, args.parity_rows)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -494,10 +594,10 @@ def run_sharded(args):
 
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = torch.device("cuda", local)
     from paper_2504_07264_b200 import _ffi
     from paper_2504_07264_b200 import dist as sdist
+    sdist.init_process_group("nccl", device=torch.device("cuda", local))
+    device = torch.device("cuda", local)
 
     cfg = workloads.CONFIGS[args.config]
     dt = torch.float32 if cfg.dtype == "f32" else torch.float64
@@ -547,7 +647,10 @@ def run_sharded(args):
     ms = float(ms_t.item())
     if rank == 0:
         peak, src = peaks()
-        moved = 2 * len(plan_groups(cfg.log2n)) * 2 * nl * (4 if cfg.dtype == "f32" else 8)
+        # per-rank HBM bytes: every pass launch of the C dist plan reads and
+        # writes the rank's N/G elements of both planes once
+        sweeps = sum(plan.launches)
+        moved = sweeps * 2 * 2 * nl * (4 if cfg.dtype == "f32" else 8)
         line = {
             "metric": BASELINE_METRIC, "value": 1.0 / (ms / 1e3), "unit": "transforms/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -559,7 +662,9 @@ def run_sharded(args):
             "gbs_algorithmic": 4 * cfg.n * (4 if cfg.dtype == "f32" else 8) / (ms / 1e3) / 1e9,
             "roofline": {"bound": "hbm", "achieved": moved / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": moved / (ms / 1e3) / 1e9 / peak, "traffic": None,
-                         "note": "per-rank HBM bytes of all pass launches / step time (includes the all-to-all)",
+                         "sweeps_per_step": sweeps, "launches_per_phase": list(plan.launches),
+                         "note": "per-rank HBM bytes of all pass launches (C dist plan) / step time "
+                                 "(includes the all-to-all)",
                          "peak_source": src},
             "gpu_launches": int(launches), "clocks": clocks.summary(),
         }
@@ -567,14 +672,26 @@ def run_sharded(args):
     dist.destroy_process_group()
 
 
-def plan_groups(m):
-    g = (m + 8) // 9
-    return [m // g + (1 if k < m % g else 0) for k in range(g)]
+def free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args):
+    """--gpus N without a launcher: re-run this script under torchrun with N
+    ranks (one per GPU) and pass rank 0's line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)]
+    cmd += [a for a in sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
     world, _, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     elif world > 1 and workloads.CONFIGS[args.config].batch == 1:

@@ -67,10 +67,15 @@ def fft_split_c(x_re, x_im, algorithm="dit", inverse=False, threads=None):
     yr = np.empty_like(xr)
     yi = np.empty_like(xi)
     if threads is None:
-        threads = min(os.cpu_count() or 1, max(1, b))
+        # rows split across threads; fewer rows than cores and m >= 16: the
+        # threads split each stage of a row instead (bit-identical)
+        threads = os.cpu_count() or 1 if (b < (os.cpu_count() or 1) and m >= 16) else \
+            min(os.cpu_count() or 1, max(1, b))
     rc = lib().oracle_fft_split(m, 1 if algorithm == "dif" else 0, 1 if inverse else 0,
                                 xr.ctypes.data, xi.ctypes.data, yr.ctypes.data, yi.ctypes.data,
                                 b, n, n, int(threads))
+    if rc == 2:
+        raise MemoryError("oracle: out of host memory")
     if rc:
         raise ValueError("oracle rejected the arguments")
     if one:

@@ -211,9 +211,168 @@ static void *run_rows(void *arg)
     return NULL;
 }
 
+/* ---- one long signal over many threads ------------------------------------
+ * For batches smaller than the thread count (config 5: one 2^28-point
+ * signal) the threads split the work INSIDE each stage instead of across
+ * rows: every stage's n/2 butterflies are independent (transform.py:131-150
+ * updates disjoint (a, b) pairs), so thread t takes a contiguous range of
+ * butterfly indices, and a barrier separates the stages -- the same
+ * operations on the same values in the same stage order, hence bit-identical
+ * to one_signal().  The gather, stage 1 and the (de)interleave split by
+ * element ranges the same way. */
+typedef struct {
+    const job_t *j;
+    int tid, nth;
+    double *z, *s;
+    int64_t row;
+    pthread_barrier_t *bar;
+} wide_t;
+
+static void range_of(int64_t total, int tid, int nth, int64_t *lo, int64_t *hi)
+{
+    int64_t per = (total + nth - 1) / nth;
+    *lo = (int64_t)tid * per < total ? (int64_t)tid * per : total;
+    *hi = *lo + per < total ? *lo + per : total;
+}
+
+static void *wide_worker(void *arg)
+{
+    wide_t *w = (wide_t *)arg;
+    const job_t *j = w->j;
+    const int m = j->m;
+    const int64_t n = 1LL << m;
+    double *z = w->z, *s = w->s;
+    int64_t lo, hi;
+    const int64_t r = w->row;
+    const double scale = 1.0 / (double)n;
+    /* interleave (layout.py:89-101; ifft swaps channels first, :280-283) */
+    range_of(n, w->tid, w->nth, &lo, &hi);
+    const double *xr = j->x_re + r * j->in_stride, *xi = j->x_im + r * j->in_stride;
+    for (int64_t k = lo; k < hi; ++k) {
+        z[2 * k] = j->inverse ? xi[k] : xr[k];
+        z[2 * k + 1] = j->inverse ? xr[k] : xi[k];
+    }
+    pthread_barrier_wait(w->bar);
+    if (j->algo == 0) {
+        for (int64_t k = lo; k < hi; ++k) {                  /* gather (:217) */
+            s[2 * k] = z[2 * j->rev[k]];
+            s[2 * k + 1] = z[2 * j->rev[k] + 1];
+        }
+        pthread_barrier_wait(w->bar);
+        range_of(n / 2, w->tid, w->nth, &lo, &hi);          /* stage 1 (:218) */
+        for (int64_t b = lo; b < hi; ++b) {
+            const int64_t k = 2 * b;
+            z[2 * k] = s[2 * k] + s[2 * k + 2];
+            z[2 * k + 1] = s[2 * k + 1] + s[2 * k + 3];
+            z[2 * k + 2] = s[2 * k] - s[2 * k + 2];
+            z[2 * k + 3] = s[2 * k + 1] - s[2 * k + 3];
+        }
+        for (int i = 2; i <= m; ++i) {                        /* stages 2..m (:131-139) */
+            pthread_barrier_wait(w->bar);
+            const int64_t h = 1LL << (i - 1);
+            const int sh = m - i;
+            for (int64_t b = lo; b < hi; ++b) {
+                const int64_t q = b & (h - 1), b0 = (b >> (i - 1)) << i;
+                double *a = z + 2 * (b0 + q), *bb = z + 2 * (b0 + q + h);
+                double tr, ti;
+                cmul(bb[0], bb[1], j->wr[q << sh], j->wi[q << sh], &tr, &ti);
+                bb[0] = a[0] - tr; bb[1] = a[1] - ti;
+                a[0] = a[0] + tr; a[1] = a[1] + ti;
+            }
+        }
+        pthread_barrier_wait(w->bar);
+    } else {
+        range_of(n / 2, w->tid, w->nth, &lo, &hi);
+        for (int i = m; i >= 2; --i) {                        /* stages m..2 (:142-150) */
+            const int64_t h = 1LL << (i - 1);
+            const int sh = m - i;
+            for (int64_t b = lo; b < hi; ++b) {
+                const int64_t q = b & (h - 1), b0 = (b >> (i - 1)) << i;
+                double *a = z + 2 * (b0 + q), *bb = z + 2 * (b0 + q + h);
+                double tr = a[0] - bb[0], ti = a[1] - bb[1];
+                a[0] = a[0] + bb[0]; a[1] = a[1] + bb[1];
+                cmul(tr, ti, j->wr[q << sh], j->wi[q << sh], &bb[0], &bb[1]);
+            }
+            pthread_barrier_wait(w->bar);
+        }
+        for (int64_t b = lo; b < hi; ++b) {                   /* stage 1 into scratch (:268) */
+            const int64_t k = 2 * b;
+            s[2 * k] = z[2 * k] + z[2 * k + 2];
+            s[2 * k + 1] = z[2 * k + 1] + z[2 * k + 3];
+            s[2 * k + 2] = z[2 * k] - z[2 * k + 2];
+            s[2 * k + 3] = z[2 * k + 1] - z[2 * k + 3];
+        }
+        pthread_barrier_wait(w->bar);
+        range_of(n, w->tid, w->nth, &lo, &hi);
+        for (int64_t k = lo; k < hi; ++k) {                   /* gather (:269) */
+            z[2 * k] = s[2 * j->rev[k]];
+            z[2 * k + 1] = s[2 * j->rev[k] + 1];
+        }
+        pthread_barrier_wait(w->bar);
+    }
+    range_of(n, w->tid, w->nth, &lo, &hi);
+    double *yr = j->y_re + r * j->out_stride, *yi = j->y_im + r * j->out_stride;
+    for (int64_t k = lo; k < hi; ++k) {
+        if (j->inverse) {               /* swap back, then data *= 1/N (:296-297) */
+            yr[k] = z[2 * k + 1] * scale;
+            yi[k] = z[2 * k] * scale;
+        } else {
+            yr[k] = z[2 * k];
+            yi[k] = z[2 * k + 1];
+        }
+    }
+    return NULL;
+}
+
+typedef struct {
+    int m, tid, nth;
+    double *wr, *wi;
+    int64_t *rev;
+} tab_t;
+
+static void *table_worker(void *arg)
+{
+    tab_t *t = (tab_t *)arg;
+    const int64_t n = 1LL << t->m, h = n / 2;
+    int64_t lo, hi;
+    range_of(h, t->tid, t->nth, &lo, &hi);
+    for (int64_t q = lo; q < hi; ++q) stage_factor(t->m, q, &t->wr[q], &t->wi[q]);
+    range_of(n, t->tid, t->nth, &lo, &hi);
+    for (int64_t k = lo; k < hi; ++k) {
+        int64_t r = 0, v = k;
+        for (int b = 0; b < t->m; ++b) { r = (r << 1) | (v & 1); v >>= 1; }
+        t->rev[k] = r;
+    }
+    return NULL;
+}
+
+static int run_wide(job_t *j, int64_t batch, int threads)
+{
+    const int64_t n = 1LL << j->m;
+    double *z = (double *)malloc(sizeof(double) * 4 * (size_t)n);
+    if (!z) return 2;
+    pthread_barrier_t bar;
+    pthread_barrier_init(&bar, NULL, (unsigned)threads);
+    pthread_t *tids = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    wide_t *ws = (wide_t *)calloc((size_t)threads, sizeof(wide_t));
+    for (int64_t r = 0; r < batch; ++r) {
+        for (int t = 0; t < threads; ++t) {
+            ws[t].j = j; ws[t].tid = t; ws[t].nth = threads;
+            ws[t].z = z; ws[t].s = z + 2 * n; ws[t].row = r; ws[t].bar = &bar;
+            pthread_create(&tids[t], NULL, wide_worker, &ws[t]);
+        }
+        for (int t = 0; t < threads; ++t) pthread_join(tids[t], NULL);
+    }
+    pthread_barrier_destroy(&bar);
+    free(ws); free(tids); free(z);
+    return 0;
+}
+
 /* Batched split -> split transform of `batch` rows, fp64, over `threads`
- * POSIX threads (the reference has no internal parallelism; threads only
- * split independent rows).  algo: 0 = dit, 1 = dif.  Returns 0 on success. */
+ * POSIX threads (the reference has no internal parallelism; threads split
+ * independent rows, or -- fewer rows than threads and m >= 16 -- the
+ * butterflies of each stage of one row, run_wide).  algo: 0 = dit,
+ * 1 = dif.  Returns 0 on success. */
 int oracle_fft_split(int m, int algo, int inverse,
                      const double *x_re, const double *x_im,
                      double *y_re, double *y_im,
@@ -222,12 +381,34 @@ int oracle_fft_split(int m, int algo, int inverse,
 {
     if (m < 0 || m > ORACLE_MAX_M || batch < 0) return 1;
     if (threads < 1) threads = 1;
-    if (threads > batch) threads = batch > 0 ? (int)batch : 1;
+    const int wide = batch < threads && m >= 16;
+    if (!wide && threads > batch) threads = batch > 0 ? (int)batch : 1;
     int64_t n = 1LL << m;
     int64_t h = m >= 1 ? n / 2 : 1;
     double *wr = (double *)malloc(sizeof(double) * 2 * (size_t)h);
     double *wi = wr + h;
     int64_t *rev = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
+    if (!wr || !rev) { free(wr); free(rev); return 2; }
+    if (wide) {
+        /* tables of a long plan in parallel (same values: stage_factor per q) */
+        pthread_t *tt = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+        tab_t *ta = (tab_t *)calloc((size_t)threads, sizeof(tab_t));
+        for (int t = 0; t < threads; ++t) {
+            ta[t].m = m; ta[t].tid = t; ta[t].nth = threads; ta[t].wr = wr; ta[t].wi = wi; ta[t].rev = rev;
+            pthread_create(&tt[t], NULL, table_worker, &ta[t]);
+        }
+        for (int t = 0; t < threads; ++t) pthread_join(tt[t], NULL);
+        free(ta); free(tt);
+        job_t j;
+        memset(&j, 0, sizeof j);
+        j.m = m; j.algo = algo; j.inverse = inverse;
+        j.wr = wr; j.wi = wi; j.rev = rev;
+        j.x_re = x_re; j.x_im = x_im; j.y_re = y_re; j.y_im = y_im;
+        j.in_stride = in_stride; j.out_stride = out_stride;
+        int rc = run_wide(&j, batch, threads);
+        free(rev); free(wr);
+        return rc;
+    }
     if (m >= 1) oracle_twiddle_table(m, wr, wi);
     oracle_bitrev(m, rev);
     job_t *jobs = (job_t *)calloc((size_t)threads, sizeof(job_t));

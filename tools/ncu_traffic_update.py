@@ -3,6 +3,11 @@
 (mean over the captured launches).
 
     python tools/ncu_traffic_update.py cfg2_n64_f32=gpurun_out/prof_r01p_cfg2_n64_f32.ncu-rep ...
+
+The kernel-source hash is read from gpurun_out/prof_<TAG>.srchash (written
+by tools/prof_cfgs.sh on the box at capture time); bench.py only reports a
+capture whose hash matches the sources it runs.  An entry named
+"cfg:dif" records a DIF capture.
 """
 import csv
 import json
@@ -31,12 +36,18 @@ def main():
         table = json.load(f)
     for arg in sys.argv[1:]:
         cfg, rep = arg.split("=", 1)
+        algo = "dit"
+        if ":" in cfg:
+            cfg, algo = cfg.split(":", 1)
+        tag = os.path.basename(rep).split("_")[1]     # prof_<TAG>_<cfg>.ncu-rep
+        hpath = os.path.join(os.path.dirname(rep), f"prof_{tag}.srchash")
+        src = open(hpath).read().strip() if os.path.exists(hpath) else None
         ls = list(launches(rep))
         rd = sum(x[1] for x in ls) / len(ls)
         wr = sum(x[2] for x in ls) / len(ls)
         table[cfg] = {"kernel": ls[0][0][:120], "dram_bytes_read": rd, "dram_bytes_write": wr,
                       "dram_bytes_per_launch": rd + wr, "launches_captured": len(ls),
-                      "source": os.path.relpath(rep, ROOT)}
+                      "source": os.path.relpath(rep, ROOT), "src_hash": src, "algorithm": algo}
         print(cfg, len(ls), f"{(rd + wr) / 1e9:.4f} GB per launch", ls[0][0][:80])
     with open(PATH, "w") as f:
         json.dump(table, f, indent=1)

@@ -184,7 +184,8 @@ def shapes():
                     continue
                 out.add((esz, logn, lr, gen_inst.fused_nt(logn, lr)))   # LDG kernel
         for logn, cfgs in gen_inst.TMA_CONFIGS[dt].items():
-            for lr, nt, _, _ in cfgs:
+            for c in cfgs:
+                lr, nt = c[0], c[1]
                 p_ = 1 << (logn - lr)
                 out.add((esz, logn, lr, max(p_, nt)))          # TMA kernel
     return sorted(out)

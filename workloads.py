@@ -64,18 +64,33 @@ CONFIGS = {
 _CHUNK_ELEMS = 1 << 24
 
 
-def _draw_plane(rng, dist, batch, n, rows, out_dtype):
-    """Draw a (batch, n) float64 plane in row chunks; keep the first `rows`."""
+def _draw_plane(rng, dist, batch, n, rows, out_dtype, start=0):
+    """Draw a (batch, n) float64 plane in row chunks; keep rows
+    [start, start + rows)."""
     out = np.empty((rows, n), dtype=out_dtype)
     step = max(1, _CHUNK_ELEMS // n)
+    end = start + rows
+    if dist == "uniform":
+        # uniform doubles take exactly one 64-bit draw each (PCG64
+        # next_double), so rows outside [start, end) are skipped by advancing
+        # the generator instead of drawing them: the same stream, checked in
+        # tests/test_workloads.py
+        bg = rng.bit_generator
+        bg.advance(start * n)
+        for r0 in range(start, end, step):
+            r1 = min(end, r0 + step)
+            out[r0 - start:r1 - start] = rng.uniform(-1.0, 1.0, (r1 - r0, n))
+        bg.advance((batch - end) * n)
+        return out
     for r0 in range(0, batch, step):
         r1 = min(batch, r0 + step)
         if dist == "uniform":
             blk = rng.uniform(-1.0, 1.0, (r1 - r0, n))
         else:
             blk = rng.standard_normal((r1 - r0, n))
-        if r0 < rows:
-            out[r0:min(r1, rows)] = blk[: min(r1, rows) - r0]
+        lo, hi = max(r0, start), min(r1, end)
+        if lo < hi:
+            out[lo - start:hi - start] = blk[lo - r0:hi - r0]
     return out
 
 
@@ -86,22 +101,26 @@ def tone_params(cfg: Config, rng):
     return k, amp, phi
 
 
-def generate(cfg: Config, rows=None, dtype=None):
-    """(x_re, x_im) numpy arrays of shape (rows, N) (rows defaults to B).
+def generate(cfg: Config, rows=None, dtype=None, start=0):
+    """(x_re, x_im) numpy arrays of shape (rows, N): rows [start, start+rows)
+    of the config's stream (rows defaults to B - start).
 
     Values are computed in float64 and cast to the config dtype (or `dtype`).
     """
-    rows = cfg.batch if rows is None else min(rows, cfg.batch)
+    if not 0 <= start <= cfg.batch:
+        raise ValueError(f"start row {start} outside [0, {cfg.batch}]")
+    rows = cfg.batch - start if rows is None else min(rows, cfg.batch - start)
     out_dtype = dtype or cfg.np_dtype
     rng = np.random.default_rng(cfg.seed)
     if cfg.dist in ("uniform", "normal"):
-        re = _draw_plane(rng, cfg.dist, cfg.batch, cfg.n, rows, out_dtype)
-        im = _draw_plane(rng, cfg.dist, cfg.batch, cfg.n, rows, out_dtype)
+        re = _draw_plane(rng, cfg.dist, cfg.batch, cfg.n, rows, out_dtype, start)
+        im = _draw_plane(rng, cfg.dist, cfg.batch, cfg.n, rows, out_dtype, start)
         return re, im
     # structured tones (config 4)
     k, amp, phi = tone_params(cfg, rng)
-    noise_re = _draw_plane(rng, "normal", cfg.batch, cfg.n, rows, np.float64)
-    noise_im = _draw_plane(rng, "normal", cfg.batch, cfg.n, rows, np.float64)
+    k, amp, phi = k[start:start + rows], amp[start:start + rows], phi[start:start + rows]
+    noise_re = _draw_plane(rng, "normal", cfg.batch, cfg.n, rows, np.float64, start)
+    noise_im = _draw_plane(rng, "normal", cfg.batch, cfg.n, rows, np.float64, start)
     n = cfg.n
     ang = 2.0 * np.pi * np.arange(n) / n
     table = np.cos(ang) + 1j * np.sin(ang)
