@@ -127,6 +127,21 @@ int sfft_exec_interleaved(const sfft_plan *plan, const void *x, void *y,
                           int64_t batch, int64_t in_stride, int64_t out_stride,
                           int direction, void *workspace, void *stream);
 
+/* The literal per-stage operators on the interleaved layout, in place,
+ * batched over `batch` rows of 2^log2n (re, im) pairs (stride in pairs):
+ * butterfly_stage W^(i) -- within each block of 2^i pairs, pair q and pair
+ * q + 2^(i-1) become their sum and difference (transform.py:88-101) -- and
+ * twiddle_stage D^(i) -- pair q >= 1 of each block's second half is
+ * multiplied by the plan's stage-i factor w_i[q], the identity column left
+ * untouched (transform.py:104-120; stage 1 is the identity).  Composed with
+ * the pairwise bit reversal they reproduce fft_dit / fft_dif bit for bit
+ * (fp64).  EINVAL "stage index i out of range for m=..." as the reference. */
+int sfft_exec_butterfly_stage(int dtype, int log2n, int stage, void *data,
+                              int64_t batch, int64_t stride, int device,
+                              void *stream);
+int sfft_exec_twiddle_stage(const sfft_plan *plan, int stage, void *data,
+                            int64_t batch, int64_t stride, void *stream);
+
 /* ---- one transform sharded over nranks GPUs (four-step, one all-to-all) ----
  * N = 2^log2n = N1 * N2 with N1 = 2^floor(log2n/2).  Data distribution
  * (G = nranks, power of two; rank g):

@@ -27,6 +27,7 @@ from .transform import (
     Algorithm,
     FftPlan,
     FlopReport,
+    butterfly_stage,
     count_flops,
     fft,
     fft_dif,
@@ -35,6 +36,7 @@ from .transform import (
     ifft,
     ifft_split,
     make_plan,
+    twiddle_stage,
 )
 from .twiddle import RotationBlock, RotationKind, build_twiddle_table, rotation_block
 
@@ -51,6 +53,7 @@ __all__ = [
     "bit_reverse_index",
     "bit_reverse_indices",
     "build_twiddle_table",
+    "butterfly_stage",
     "count_flops",
     "deinterleave",
     "fft",
@@ -64,5 +67,6 @@ __all__ = [
     "make_plan",
     "permute_pairwise_bitrev",
     "rotation_block",
+    "twiddle_stage",
     "__version__",
 ]

@@ -36,6 +36,8 @@ SIGNATURES = {
     "sfft_exec_schedule": (_I, [_P, _I64, _I, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "sfft_exec_split": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I, _P, _P]),
     "sfft_exec_interleaved": (_I, [_P, _P, _P, _I64, _I64, _I64, _I, _P, _P]),
+    "sfft_exec_butterfly_stage": (_I, [_I, _I, _I, _P, _I64, _I64, _I, _P]),
+    "sfft_exec_twiddle_stage": (_I, [_P, _I, _P, _I64, _I64, _P]),
     "sfft_twiddle_table": (_I, [_I, _P, _P]),
     "sfft_count_flops": (_I, [_I, ctypes.POINTER(_I64)]),
     "sfft_launch_count": (_I64, []),

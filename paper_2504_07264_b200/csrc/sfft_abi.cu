@@ -24,6 +24,7 @@
 #include "sfft_fused.cuh"
 #include "sfft_launch.h"
 #include "sfft_pass.cuh"
+#include "sfft_stage.cuh"
 #include "sfft_tma_host.h"
 
 #include <mutex>
@@ -607,6 +608,62 @@ int sfft_exec_split(const sfft_plan *plan, const void *x_re, const void *x_im, v
 {
     return exec_common(plan, x_re, x_im, y_re, y_im, false, batch, in_stride, out_stride, direction, workspace,
                        stream);
+}
+
+// transform.py:88-120 (butterfly_stage / twiddle_stage) on the interleaved
+// layout, batched over rows; see sfft_stage.cuh.
+static int exec_stage(int kind, int dtype, int log2n, int stage, const sfft_plan *p, void *data, int64_t batch,
+                      int64_t stride, int device, void *stream)
+{
+    if (log2n < 0 || log2n > SFFT_MAX_LOG2N) return fail(SFFT_EINVAL, "stage count m must be >= 0, got %d", log2n);
+    if (stage < 1 || stage > log2n) return fail(SFFT_EINVAL, "stage index %d out of range for m=%d", stage, log2n);
+    if (dtype != SFFT_F32 && dtype != SFFT_F64) return fail(SFFT_EINVAL, "unknown dtype %d", dtype);
+    if (batch < 0) return fail(SFFT_EINVAL, "batch must be >= 0, got %lld", (long long)batch);
+    const int64_t n = int64_t(1) << log2n;
+    if (batch > 1 && stride < n) return fail(SFFT_EINVAL, "row stride %lld must be >= N = %lld", (long long)stride, (long long)n);
+    if (batch == 0 || (kind == 1 && stage == 1)) return SFFT_OK;   // the stage-1 rotation is the identity
+    if (!data) return fail(SFFT_EINVAL, "NULL data pointer");
+    if (batch > 65535) return fail(SFFT_ECAPACITY, "batch %lld exceeds one stage launch (65535 rows)", (long long)batch);
+    DeviceGuard dg(device);
+    if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+    const int64_t half = n >> 1;
+    const dim3 grid((unsigned)((half + 255) / 256), (unsigned)batch);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == SFFT_F64) {
+        TwCat<double> tw{(const double2 *)(p ? p->d_tw : nullptr)};
+        if (kind == 0) sfft_stage_kernel<double, 0><<<grid, 256, 0, st>>>((double2 *)data, stride, log2n, stage, tw);
+        else sfft_stage_kernel<double, 1><<<grid, 256, 0, st>>>((double2 *)data, stride, log2n, stage, tw);
+    } else if (kind == 0 || !p || stage <= p->cat_top) {
+        TwCat<float> tw{(const float2 *)(p ? p->d_tw : nullptr)};
+        if (kind == 0) sfft_stage_kernel<float, 0><<<grid, 256, 0, st>>>((float2 *)data, stride, log2n, stage, tw);
+        else sfft_stage_kernel<float, 1><<<grid, 256, 0, st>>>((float2 *)data, stride, log2n, stage, tw);
+    } else {
+        // fp32 plans above the stage-major table: the two-level factors the
+        // pass kernels use (sfft_common.cuh TwTwoLevel)
+        TwTwoLevel<float> tw;
+        tw.tab = (const float2 *)p->d_tw;
+        tw.cat_top = p->cat_top;
+        tw.coarse = p->d_coarse;
+        tw.coarse_log = p->coarse_log;
+        tw.fine = p->d_fine;
+        tw.m = p->log2n;
+        sfft_stage_kernel<float, 1><<<grid, 256, 0, st>>>((float2 *)data, stride, log2n, stage, tw);
+    }
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? SFFT_OK : cuda_fail(e, "stage kernel launch");
+}
+
+int sfft_exec_butterfly_stage(int dtype, int log2n, int stage, void *data, int64_t batch, int64_t stride,
+                              int device, void *stream)
+{
+    return exec_stage(0, dtype, log2n, stage, nullptr, data, batch, stride, device, stream);
+}
+
+int sfft_exec_twiddle_stage(const sfft_plan *p, int stage, void *data, int64_t batch, int64_t stride, void *stream)
+{
+    if (!p) return fail(SFFT_EINVAL, "plan is NULL");
+    return exec_stage(1, p->dtype, p->log2n, stage, p, data, batch, stride, p->device, stream);
 }
 
 int sfft_exec_interleaved(const sfft_plan *plan, const void *x, void *y, int64_t batch, int64_t in_stride,

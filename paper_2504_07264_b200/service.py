@@ -14,6 +14,7 @@ harness) are out of scope.
 from typing import List, Literal, Union
 
 import numpy as np
+import torch
 from fastapi import FastAPI, HTTPException
 from pydantic import BaseModel
 
@@ -66,7 +67,9 @@ def create_app() -> FastAPI:
         try:
             re = np.asarray(req.re, dtype=np.float64)
             im = np.asarray(req.im, dtype=np.float64)
-            sig = SplitSignal(re, im)                 # length / shape checks (layout.py:28-37)
+            # length / shape checks (layout.py:28-37); torch mode keeps the
+            # batched [B, N] request rows of this service
+            sig = SplitSignal(torch.from_numpy(re), torch.from_numpy(im))
             n = len(sig)
             if not is_power_of_two(n):
                 raise ValueError(f"sample count {n} is not a power of two")   # layout.py:96-97

@@ -236,7 +236,12 @@ def fft_split(x_re, x_im, *, algorithm="dit", inverse: bool = False, out=None, p
     ``out=(y_re, y_im)`` may alias the inputs (in place).  Returns the output
     planes in the input's container type.
     """
-    was_numpy = not isinstance(x_re, torch.Tensor)
+    was_numpy = not isinstance(x_re, torch.Tensor) and not isinstance(x_im, torch.Tensor)
+    if was_numpy:
+        # host arrays follow the reference's containers: float64 (fp32 is
+        # upcast exactly, layout.py:29-30), results returned as float64
+        x_re = torch.from_numpy(np.ascontiguousarray(x_re, dtype=np.float64))
+        x_im = torch.from_numpy(np.ascontiguousarray(x_im, dtype=np.float64))
     sig = SplitSignal(x_re, x_im)
     n = len(sig)
     if not is_power_of_two(n):
@@ -279,6 +284,8 @@ def fft_split(x_re, x_im, *, algorithm="dit", inverse: bool = False, out=None, p
         hr, hi = out
         hr = torch.from_numpy(hr) if not isinstance(hr, torch.Tensor) else hr
         hi = torch.from_numpy(hi) if not isinstance(hi, torch.Tensor) else hi
+        if hr.dtype != hr_in.dtype and was_numpy:
+            raise ValueError("out arrays for numpy input must be float64 (the reference's dtype)")
         if hr.shape != hr_in.shape or hi.shape != hr_in.shape or hr.dtype != hr_in.dtype:
             raise ValueError("out planes must match the input shape and dtype")
     else:
@@ -363,10 +370,21 @@ def _run_interleaved(plan: FftPlan, buf: InterleavedBuffer, inverse: bool, algor
         # fft_dit/fft_dif on a plan built for the other variant: same tables,
         # other kernel family (the reference's plans serve both, :208-270)
         plan = _cached_plan(plan.m, algorithm, plan.dtype, plan.device.index)
+    direction = _ffi.SFFT_INVERSE if inverse else _ffi.SFFT_FORWARD
+    if not buf.is_torch:
+        # the reference's float64 numpy buffer: transformed on the GPU in the
+        # plan's dtype and written back in place (transform.py:208-298
+        # mutate buf.data)
+        work = torch.from_numpy(buf.data).to(plan.device, plan.dtype)
+        n = plan.sample_count
+        ws, wsp = _workspace(plan, 1)
+        _ffi.check(_ffi.lib.sfft_exec_interleaved(plan._handle, work.data_ptr(), work.data_ptr(), 1, n, n,
+                                                  direction, wsp, _stream_ptr(plan.device)))
+        buf.data[...] = work.cpu().numpy()
+        return buf
     data = buf.data
     if data.dtype != plan.dtype:
         raise ValueError(f"buffer dtype {data.dtype} does not match plan dtype {plan.dtype}")
-    direction = _ffi.SFFT_INVERSE if inverse else _ffi.SFFT_FORWARD
     host = data.device.type != "cuda"
     work = data.to(plan.device, non_blocking=True) if host else data
     if work.device != plan.device:
@@ -383,6 +401,57 @@ def _run_interleaved(plan: FftPlan, buf: InterleavedBuffer, inverse: bool, algor
     if work.data_ptr() != data.data_ptr():
         data.copy_(work)
     return buf
+
+
+def _stage_operand(buf: InterleavedBuffer, device, dtype):
+    """(device tensor the stage kernel runs on, write-back) for a buffer."""
+    if not buf.is_torch:
+        work = torch.from_numpy(buf.data).to(device, dtype)
+
+        def back():
+            buf.data[...] = work.cpu().numpy()
+        return work, back
+    data = buf.data
+    if data.device.type == "cuda" and data.is_contiguous() and data.dtype == dtype:
+        return data, lambda: None
+    work = data.to(device, dtype).contiguous()
+    return work, lambda: data.copy_(work)
+
+
+def butterfly_stage(buf: InterleavedBuffer, i: int) -> None:
+    """Apply the stage-``i`` butterflies W^(i) in place (transform.py:88-101):
+    within each block of ``2**i`` pairs, pair q and pair q + 2**(i-1) become
+    their sum and difference.  Runs on the GPU (sfft_stage.cuh)."""
+    if not 1 <= i <= buf.m:
+        raise ValueError(f"stage index {i} out of range for m={buf.m}")
+    if buf.is_torch and buf.data.device.type == "cuda":
+        device, dtype = buf.data.device, buf.data.dtype
+    else:
+        device = _resolve_device(None)
+        dtype = buf.data.dtype if buf.is_torch else torch.float64
+    work, back = _stage_operand(buf, device, dtype)
+    batch = 1 if work.ndim == 1 else work.shape[0]
+    _ffi.check(_ffi.lib.sfft_exec_butterfly_stage(_DTYPE_CODE[dtype], buf.m, int(i), work.data_ptr(), batch,
+                                                  buf.sample_count, device.index, _stream_ptr(device)))
+    back()
+
+
+def twiddle_stage(buf: InterleavedBuffer, plan: FftPlan, i: int) -> None:
+    """Apply the stage-``i`` rotations D^(i) in place (transform.py:104-120):
+    pair q >= 1 of each block's second half is multiplied by the stage-i
+    factor (the identity column is skipped, as the reference does).  Runs on
+    the GPU with the plan's tables and dtype (sfft_stage.cuh)."""
+    if buf.m != plan.m:
+        raise ValueError(f"buffer is for m={buf.m} but plan is for m={plan.m}")
+    if not 1 <= i <= plan.m:
+        raise ValueError(f"stage index {i} out of range for m={plan.m}")
+    if i == 1:
+        return  # the single stage-1 rotation is the identity
+    work, back = _stage_operand(buf, plan.device, plan.dtype)
+    batch = 1 if work.ndim == 1 else work.shape[0]
+    _ffi.check(_ffi.lib.sfft_exec_twiddle_stage(plan._handle, int(i), work.data_ptr(), batch, plan.sample_count,
+                                                _stream_ptr(plan.device)))
+    back()
 
 
 def fft_dit(plan: FftPlan, buf: InterleavedBuffer) -> InterleavedBuffer:

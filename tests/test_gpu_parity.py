@@ -324,3 +324,81 @@ def test_cuda_graph_capture_and_replay(cuda, m):
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(yr, want[0]) and torch.equal(yi, want[1])
+
+
+# ---- the GPU pinned straight to the reference at m > 14 (no oracle in the
+# loop): SHA-256 of the fp64 output bytes equals the reference's
+# (tests/golden/reference_large_pins.json; the reference's stage-pair slab
+# path, transform.py:160-200, 227-237)
+def _large_pins():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "reference_large_pins.json")) as f:
+        return json.load(f)["pins"]
+
+
+@pytest.mark.parametrize("tag", sorted(_large_pins()))
+def test_gpu_fp64_large_m_matches_reference_digest(cuda, tag):
+    import hashlib
+    pin = _large_pins()[tag]
+    m = int(tag.split("_")[0][1:])
+    algo, inv = tag.split("_")[1], tag.endswith("inv")
+    rng = np.random.default_rng(5000 + m)
+    re, im = rng.standard_normal(1 << m), rng.standard_normal(1 << m)
+    plan = sf.make_plan(m, algo, dtype=torch.float64, device="cuda:0")
+    yr, yi = sf.fft_split(torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda(), plan=plan, inverse=inv)
+    gr, gi = yr.cpu().numpy(), yi.cpu().numpy()
+    d = lambda a: hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()   # noqa: E731
+    assert d(gr) == pin["sha256_re"] and d(gi) == pin["sha256_im"]
+
+
+# ---- the literal per-stage operators (transform.py:88-120) on the GPU ----
+@pytest.mark.parametrize("dt", ["f64", "f32"])
+@pytest.mark.parametrize("m", [1, 3, 8, 13, 14])
+def test_stage_operators_batched_torch(cuda, dt, m):
+    # batched torch buffers (the extension) equal the reference-mode numpy
+    # buffers row by row; composed with the bit reversal they give fft_dit /
+    # fft_dif (fp64: bit for bit)
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    rng = np.random.default_rng(70 + m)
+    b = 3
+    data = rng.standard_normal((b, 2 << m))
+    plan = sf.make_plan(m, "dit", dtype=tdt, device="cuda:0")
+    for i in range(1, m + 1):
+        t = sf.InterleavedBuffer(torch.from_numpy(data).to("cuda:0", tdt), m)
+        sf.butterfly_stage(t, i)
+        sf.twiddle_stage(t, plan, i)
+        for r in range(b):
+            nb = sf.InterleavedBuffer(data[r].astype(np.float32 if dt == "f32" else np.float64), m)
+            sf.butterfly_stage(nb, i)
+            sf.twiddle_stage(nb, plan, i)
+            got = t.data[r].cpu().numpy().astype(np.float64)
+            if dt == "f64":
+                assert np.array_equal(got, nb.data)
+            else:
+                assert np.max(np.abs(got - nb.data)) <= 1e-5 * (1 + np.abs(nb.data).max())
+    if dt == "f64":
+        sig = sf.SplitSignal(data[0, 0::2].copy(), data[0, 1::2].copy())
+        fast = sf.interleave(sig)
+        sf.fft_dit(plan, fast)
+        slow = sf.permute_pairwise_bitrev(sf.interleave(sig))
+        for i in range(1, m + 1):
+            sf.twiddle_stage(slow, plan, i)
+            sf.butterfly_stage(slow, i)
+        assert np.array_equal(fast.data, slow.data)
+
+
+def test_numpy_containers_follow_the_reference(cuda):
+    # fp32 numpy input is upcast to float64 and computed in fp64, like
+    # layout.py:29-30 -- through the default plan and through fft_split
+    rng = np.random.default_rng(3)
+    re = rng.standard_normal(256).astype(np.float32)
+    im = rng.standard_normal(256).astype(np.float32)
+    buf = sf.interleave(sf.SplitSignal(re, im))
+    assert buf.data.dtype == np.float64
+    sf.fft(sf.make_plan(8), buf)
+    out = sf.deinterleave(buf)
+    wr, wi = oracle.fft_split_c(re.astype(np.float64), im.astype(np.float64))
+    assert np.array_equal(out.re, wr) and np.array_equal(out.im, wi)
+    yr, yi = sf.fft_split(re, im)
+    assert yr.dtype == np.float64 and np.array_equal(yr, wr) and np.array_equal(yi, wi)

@@ -83,7 +83,12 @@ def test_split_signal_validation():
     with pytest.raises(ValueError, match="one-dimensional"):
         sf.SplitSignal(np.zeros((2, 2, 2)), np.zeros((2, 2, 2)))
     s = sf.SplitSignal([1, 2], [3, 4])
-    assert s.re.dtype == torch.float64     # non-float input coerced like layout.py:29-30
+    assert s.re.dtype == np.float64         # non-torch input: the reference's container (layout.py:29-30)
+    assert sf.SplitSignal(np.ones(4, dtype=np.float32), np.ones(4)).re.dtype == np.float64
+    with pytest.raises(ValueError, match="one-dimensional"):
+        sf.SplitSignal(np.zeros((2, 4)), np.zeros((2, 4)))       # numpy: 1-D only, as the reference
+    t = sf.SplitSignal(torch.zeros(2, 4, dtype=torch.float32), torch.zeros(2, 4, dtype=torch.float32))
+    assert t.re.dtype == torch.float32 and t.batch == 2          # torch: the batched extension
     with pytest.raises(ValueError, match="not a power of two"):
         sf.interleave(sf.SplitSignal(np.zeros(6), np.zeros(6)))
     with pytest.raises(ValueError, match="does not match m"):
@@ -97,10 +102,14 @@ def test_interleave_round_trip_is_bitwise():
     re[3] = -0.0
     im[5] = 5e-324
     buf = sf.interleave(sf.SplitSignal(re, im))
-    assert buf.data[0::2].numpy().tolist() == re.tolist()
+    assert buf.data[0::2].tolist() == re.tolist()
     back = sf.deinterleave(buf)
-    assert same_bits(back.re.numpy(), re) and same_bits(back.im.numpy(), im)
-    assert np.signbit(back.re.numpy()[3])
+    assert same_bits(back.re, re) and same_bits(back.im, im)
+    assert np.signbit(back.re[3])
+    # torch containers: the same bits
+    tb = sf.interleave(sf.SplitSignal(torch.from_numpy(re), torch.from_numpy(im)))
+    tback = sf.deinterleave(tb)
+    assert same_bits(tback.re.numpy(), re) and same_bits(tback.im.numpy(), im)
 
 
 def test_bit_reverse_helpers():

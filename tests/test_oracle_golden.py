@@ -74,3 +74,33 @@ def test_golden_known_answer_4_point():
     # the reference's printed example (test_transform.py:57-62): sanity of the file itself
     yr, yi = oracle.fft_split_c(np.array([1.0, 2.0, 3.0, 4.0]), np.zeros(4))
     assert yr.tolist() == [10.0, -2.0, -2.0, -2.0] and yi.tolist() == [0.0, 2.0, 0.0, -2.0]
+
+
+# ---- m > 14: the reference's stage-pair slab path (transform.py:160-200,
+# 227-237), pinned by SHA-256 of the reference's output bytes
+# (tests/golden/reference_large_pins.json, written by make_golden.py --large)
+import hashlib  # noqa: E402
+import json  # noqa: E402
+
+LARGE = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_large_pins.json")))["pins"]
+
+
+def large_input(m):
+    rng = np.random.default_rng(5000 + m)
+    return rng.standard_normal(1 << m), rng.standard_normal(1 << m)
+
+
+def digest(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype="<f8").tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("tag", sorted(LARGE))
+def test_c_oracle_large_m_pins(tag):
+    m = int(tag.split("_")[0][1:])
+    algo, inv = tag.split("_")[1], tag.endswith("inv")
+    re, im = large_input(m)
+    yr, yi = oracle.fft_split_c(re, im, algo, inv)
+    pin = LARGE[tag]
+    idx = np.array(pin["sample_index"])
+    assert same_bits(yr[idx], np.array(pin["sample_re"])) and same_bits(yi[idx], np.array(pin["sample_im"]))
+    assert digest(yr) == pin["sha256_re"] and digest(yi) == pin["sha256_im"]
