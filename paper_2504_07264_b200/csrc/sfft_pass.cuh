@@ -214,18 +214,22 @@ __device__ __forceinline__ typename PassTw<T, S0>::type make_pass_tw(const PassA
 // per SM, measured 3-4% slower on N = 2^28 even though the cap spills 20
 // bytes).  fp64: 0 = no minimum (the compiler's choice; 1 would let it take
 // up to 233 registers).
-template <typename T, int L, int LR>
+// The address-map variants (sharded DIST launches, interleaved output) carry
+// more live address state: at the 64-register cap they spilled 20-28 bytes
+// per thread, so they take 3 CTAs of 256 (<= 85 registers) instead.
+template <typename T, int L, int LR, bool WIDE = false>
 struct PassMinBlocks {
     static constexpr int NT = PassShape<T, L, LR>::NT;
-    static constexpr int value = sizeof(T) == 4 ? (1024 / NT < 1 ? 1 : (1024 / NT > 8 ? 8 : 1024 / NT)) : 0;
+    static constexpr int TPS = WIDE ? 768 : 1024;    // threads per SM to fit
+    static constexpr int value = sizeof(T) == 4 ? (TPS / NT < 1 ? 1 : (TPS / NT > 8 ? 8 : TPS / NT)) : 0;
 };
 #ifdef SFFT_PASS_MINB
-#define SFFT_PASS_LB(T, L, LR) __launch_bounds__(PassShape<T, L, LR>::NT, SFFT_PASS_MINB)
+#define SFFT_PASS_LB(T, L, LR, WIDE) __launch_bounds__(PassShape<T, L, LR>::NT, SFFT_PASS_MINB)
 #else
-#define SFFT_PASS_LB(T, L, LR) __launch_bounds__(PassShape<T, L, LR>::NT, (PassMinBlocks<T, L, LR>::value))
+#define SFFT_PASS_LB(T, L, LR, WIDE) __launch_bounds__(PassShape<T, L, LR>::NT, (PassMinBlocks<T, L, LR, WIDE>::value))
 #endif
 template <typename T, int L, int LR_REQ, bool DIF, bool IL_IN, bool IL_OUT, bool S0, bool DIST>
-__global__ void SFFT_PASS_LB(T, L, LR_REQ)
+__global__ void SFFT_PASS_LB(T, L, LR_REQ, DIST || IL_OUT)
 sfft_pass_kernel(const PassArgs a)
 {
     using Sh = PassShape<T, L, LR_REQ>;

@@ -15,7 +15,7 @@ from oracle import oracle  # noqa: E402
 rng = np.random.default_rng(0)
 cases = [(6, np.float32, "tma", 700), (10, np.float32, "ldg", 40), (10, np.float64, "ldg", 40),
          (8, np.float64, "tma", 300), (12, np.float32, "ldg", 5), (14, np.float32, "auto", 2),
-         (14, np.float64, "auto", 2), (3, np.float64, "ldg", 100)]
+         (14, np.float64, "auto", 2), (3, np.float64, "ldg", 100), (10, np.float64, "tma", 300)]
 for m, dt, kern, b in cases:
     for algo in ("dit", "dif"):
         re = rng.standard_normal((b, 1 << m)).astype(dt)
@@ -26,6 +26,19 @@ for m, dt, kern, b in cases:
         gr, gi = yr.cpu().numpy().astype(np.float64), yi.cpu().numpy().astype(np.float64)
         err = np.sqrt(np.sum((gr - wr) ** 2 + (gi - wi) ** 2) / np.sum(wr ** 2 + wi ** 2))
         assert err <= 1e-5 * m, (m, dt, kern, algo, err)
+# the headline kernel (fp64 N = 1024 TMA, hoisted factors, partial exchange): inverse too
+re = rng.standard_normal((300, 1024))
+im = rng.standard_normal((300, 1024))
+for algo in ("dit", "dif"):
+    yr, yi = sf.fft_split(torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda(), algorithm=algo, inverse=True)
+    wr, wi = oracle.fft_split_c(re, im, algo, True)
+    assert np.array_equal(yr.cpu().numpy(), wr) and np.array_equal(yi.cpu().numpy(), wi)
+# per-stage operators
+buf = sf.InterleavedBuffer(torch.from_numpy(rng.standard_normal((3, 2 << 9))).cuda(), 9)
+p9 = sf.make_plan(9)
+for i in range(1, 10):
+    sf.twiddle_stage(buf, p9, i)
+    sf.butterfly_stage(buf, i)
 # interleaved
 data = torch.from_numpy(rng.standard_normal((4, 2 << 10))).cuda()
 buf = sf.InterleavedBuffer(data, 10)
