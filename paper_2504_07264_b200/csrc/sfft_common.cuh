@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "sfft_layouts.h"
 #include "sfft_small_tw.h"
 
@@ -337,6 +339,12 @@ __device__ __forceinline__ vec2_t<T> stage_factor(int t, int f, int i, bool firs
     return tw.get(i, cbase + ((I)f << gs));
 }
 
+// No factor provider (see dit_stages' `fp`).
+struct NoFP {
+    template <typename V>
+    __device__ __forceinline__ void fetch(int, V *) const {}
+};
+
 // K consecutive DIT stages (global stages gs+1 .. gs+K) on the 2^K complex
 // values v[0..2^K) (re, im) of one virtual thread.  Register position p
 // holds, before stage t, the (size 2^(gs+t-1)) partial transform of
@@ -350,16 +358,27 @@ __device__ __forceinline__ vec2_t<T> stage_factor(int t, int f, int i, bool firs
 // `hw` (optional): every factor of the K stages already in registers, stage
 // t's 2^(t-1) factors at hw[2^(t-1) - 1 + f] (the persistent kernels load
 // them once per thread for all tiles -- the factors depend on the thread's
-// column only -- so no table read sits in the tile loop).
-template <typename T, int K, bool TRIV = true, bool PACK = true, typename TW>
+// column only -- so no table read sits in the tile loop); only stages
+// t <= HK come from `hw`, the rest from the table.
+// `fp` (optional, replaces hw/table for passes after the first): a factor
+// provider whose fetch(t, w) fills w[f], f < 2^(t-1), with stage t's factors
+// once per stage before they are used (e.g. factors parked in tensor memory,
+// sfft_tma_warp.cuh).
+template <typename T, int K, bool TRIV = true, bool PACK = true, int HK = 99, typename TW, typename FP = NoFP>
 __device__ __forceinline__ void dit_stages(vec2_t<T> *v, int gs, typename TW::index_t cbase, const TW &tw,
-                                           const vec2_t<T> *pre = nullptr, const vec2_t<T> *hw = nullptr)
+                                           const vec2_t<T> *pre = nullptr, const vec2_t<T> *hw = nullptr,
+                                           const FP *fp = nullptr)
 {
+    constexpr bool HAS_FP = !std::is_same<FP, NoFP>::value;
     const bool first = TRIV && gs == 0;   // first pass: every factor is a compile-time constant
 #pragma unroll
     for (int t = 1; t <= K; ++t) {
         const int half = (1 << K) >> t;
         const int i = gs + t;
+        vec2_t<T> wf[HAS_FP ? (1 << (K - 1)) : 1];
+        if constexpr (HAS_FP) {
+            if (!first) fp->fetch(t, wf);
+        }
         vec2_t<T> base;
         if (!first && FactorTw<T>::value) base = pre ? pre[t - 1] : tw.get(i, cbase);
 #pragma unroll
@@ -372,7 +391,12 @@ __device__ __forceinline__ void dit_stages(vec2_t<T> *v, int gs, typename TW::in
                            : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w, wq;
             if (kind == 3) {
-                w = (hw && !first) ? hw[(1 << (t - 1)) - 1 + f] : stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                if constexpr (HAS_FP) {
+                    w = first ? stage_factor<T>(t, f, i, first, cbase, gs, tw, base) : wf[f];
+                } else {
+                    w = (hw && !first && t <= HK) ? hw[(1 << (t - 1)) - 1 + f]
+                                                  : stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                }
                 wq = wquad<T>(w);
             }
 #pragma unroll
@@ -396,15 +420,21 @@ __device__ __forceinline__ void dit_stages(vec2_t<T> *v, int gs, typename TW::in
 
 // Transpose of dit_stages: DIF stages gs+K .. gs+1 (descending), same
 // register map run backwards.
-template <typename T, int K, bool TRIV = true, bool PACK = true, typename TW>
+template <typename T, int K, bool TRIV = true, bool PACK = true, int HK = 99, typename TW, typename FP = NoFP>
 __device__ __forceinline__ void dif_stages(vec2_t<T> *v, int gs, typename TW::index_t cbase, const TW &tw,
-                                           const vec2_t<T> *pre = nullptr, const vec2_t<T> *hw = nullptr)
+                                           const vec2_t<T> *pre = nullptr, const vec2_t<T> *hw = nullptr,
+                                           const FP *fp = nullptr)
 {
+    constexpr bool HAS_FP = !std::is_same<FP, NoFP>::value;
     const bool first = TRIV && gs == 0;
 #pragma unroll
     for (int t = K; t >= 1; --t) {
         const int half = (1 << K) >> t;
         const int i = gs + t;
+        vec2_t<T> wf[HAS_FP ? (1 << (K - 1)) : 1];
+        if constexpr (HAS_FP) {
+            if (!first) fp->fetch(t, wf);
+        }
         vec2_t<T> base;
         if (!first && FactorTw<T>::value) base = pre ? pre[t - 1] : tw.get(i, cbase);
 #pragma unroll
@@ -416,7 +446,12 @@ __device__ __forceinline__ void dif_stages(vec2_t<T> *v, int gs, typename TW::in
                            : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
             vec2_t<T> w, wq;
             if (kind == 3) {
-                w = (hw && !first) ? hw[(1 << (t - 1)) - 1 + f] : stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                if constexpr (HAS_FP) {
+                    w = first ? stage_factor<T>(t, f, i, first, cbase, gs, tw, base) : wf[f];
+                } else {
+                    w = (hw && !first && t <= HK) ? hw[(1 << (t - 1)) - 1 + f]
+                                                  : stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                }
                 wq = wquad<T>(w);
             }
 #pragma unroll

@@ -17,10 +17,21 @@
 // addresses are padded by one element per R (phys = e + e/R) which makes
 // both exchange patterns bank-conflict free for the shipped radix choices.
 #pragma once
+#include <type_traits>
+
 #include "sfft_common.cuh"
 
 namespace sfft {
 
+// fp32 exchanges as (re, im) pairs (see Exch): one 64-bit shared access per
+// complex value.  cfg4 (N = 4096, issue-bound on LSU instructions) +4..8%,
+// N = 1024 radix 32 neutral (profiles/r02i_ab_x2.txt); -DSFFT_FUSED_NO_X2
+// restores the planar exchange for A/B builds.
+#ifdef SFFT_FUSED_NO_X2
+template <typename T> struct FusedX2 { static constexpr bool value = false; };
+#else
+template <typename T> struct FusedX2 { static constexpr bool value = sizeof(T) == 4; };
+#endif
 
 struct FusedArgs {
     const void *x0, *x1;   // planar: re, im planes; interleaved: x0 = pairs
@@ -136,10 +147,57 @@ struct FusedShape {
     static constexpr int MINB = 3;
 #endif
     static constexpr int NPASS = LOGN == 0 ? 0 : (LOGN + LR - 1) / LR;
+    // per-signal stride of the exchange (elements of one plane, or (re, im)
+    // pairs when FusedX2: then the 8-byte layouts of the same shape apply)
     template <typename T>
-    static constexpr int sstr() { return LOGN == 0 ? 1 : ex_sstr<T, LOGN, LR, NT>(); }   // per-signal plane stride
+    static constexpr int sstr()
+    {
+        if constexpr (FusedX2<T>::value) return LOGN == 0 ? 1 : ex_sstr<double, LOGN, LR, NT>();
+        else return LOGN == 0 ? 1 : ex_sstr<T, LOGN, LR, NT>();
+    }
     template <typename T>
     static constexpr int smem_bytes() { return NPASS >= 2 ? 2 * S * sstr<T>() * (int)sizeof(T) : 0; }
+};
+
+// The shared-memory exchange of one signal.  Planar (two T planes, 4-byte
+// slots for fp32) or, with FusedX2, (re, im) pairs in one array of 8-byte
+// slots: one LDS.64/STS.64 per complex value instead of two 32-bit
+// accesses (same bytes, half the LSU instructions), laid out by the planned
+// 8-byte layout of the same shape.  ld_r/st_r address slot ex_rd(...),
+// ld_w/st_w slot ex_wr(...).
+template <typename T, int LOGN, int LR_REQ>
+struct Exch {
+    using Sh = FusedShape<LOGN, LR_REQ>;
+    static constexpr int LR = Sh::LR, NT = Sh::NT;
+    static constexpr bool X2 = FusedX2<T>::value;
+    using LT = typename std::conditional<X2, double, T>::type;   // layout element size
+    using V = vec2_t<T>;
+    T *sr = nullptr, *si = nullptr;
+    V *sx = nullptr;
+    __device__ __forceinline__ V at(int i) const
+    {
+        if constexpr (X2) {
+            return sx[i];
+        } else {
+            V v;
+            v.x = sr[i];
+            v.y = si[i];
+            return v;
+        }
+    }
+    __device__ __forceinline__ void put(int i, V v) const
+    {
+        if constexpr (X2) {
+            sx[i] = v;
+        } else {
+            sr[i] = v.x;
+            si[i] = v.y;
+        }
+    }
+    __device__ __forceinline__ V ld_r(int x, int e, int et, int ec) const { return at(ex_rd<LT, LOGN, LR, NT>(x, e, et, ec)); }
+    __device__ __forceinline__ V ld_w(int x, int e, int et, int ec) const { return at(ex_wr<LT, LOGN, LR, NT>(x, e, et, ec)); }
+    __device__ __forceinline__ void st_r(int x, int e, int et, int ec, V v) const { put(ex_rd<LT, LOGN, LR, NT>(x, e, et, ec), v); }
+    __device__ __forceinline__ void st_w(int x, int e, int et, int ec, V v) const { put(ex_wr<LT, LOGN, LR, NT>(x, e, et, ec), v); }
 };
 
 
@@ -174,7 +232,7 @@ struct LastX {
 // ---- DIT pass p -----------------------------------------------------------
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL, false> &io,
+                                         const Exch<T, LOGN, LR_REQ> &xc, const GIO<T, IL, false> &io,
                                          const TwCat<T> &tw, const vec2_t<T> *pre)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
@@ -204,8 +262,7 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
                     if (r == G) {
                         v[u * RP + r] = own[u];
                     } else {
-                        v[u * RP + r].x = sr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];
-                        v[u * RP + r].y = si[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];
+                        v[u * RP + r] = xc.ld_r(p - 1, e, t, P * u + r * (N / RP));
                     }
                 }
             }
@@ -221,8 +278,7 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 if (valid) io.load(row, e, v[u * RP + r].x, v[u * RP + r].y);
                 else { v[u * RP + r].x = T(0); v[u * RP + r].y = T(0); }
             } else {
-                v[u * RP + r].x = sr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];
-                v[u * RP + r].y = si[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))];
+                v[u * RP + r] = xc.ld_r(p - 1, e, t, P * u + r * (N / RP));
             }
         }
     }
@@ -247,8 +303,7 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 for (int f = 0; f < RP; ++f) {
                     if (f % LX::RPL == G) continue;
                     const int e = base + NS * f;
-                    sr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, NS * f)] = v[brev(f, KP)].x;
-                    si[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, NS * f)] = v[brev(f, KP)].y;
+                    xc.st_w(p, e, et, NS * f, v[brev(f, KP)]);
                 }
             });
         } else {
@@ -259,8 +314,7 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
 #pragma unroll
             for (int f = 0; f < RP; ++f) {
                 const int e = base + NS * f;
-                sr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f)] = v[u * RP + brev(f, KP)].x;
-                si[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f)] = v[u * RP + brev(f, KP)].y;
+                xc.st_w(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f, v[u * RP + brev(f, KP)]);
             }
         }
         }
@@ -280,19 +334,19 @@ __device__ __forceinline__ void dit_pass(vec2_t<T> *v, int t, int64_t row, bool 
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dit_from(vec2_t<T> *v, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL, false> &io, const TwCat<T> &tw,
+                                         const Exch<T, LOGN, LR_REQ> &xc, const GIO<T, IL, false> &io, const TwCat<T> &tw,
                                          const vec2_t<T> *pre)
 {
     if constexpr (p < FusedShape<LOGN, LR_REQ>::NPASS) {
-        dit_pass<T, LOGN, LR_REQ, IL, p>(v, t, row, valid, sr, si, io, tw, pre);
-        dit_from<T, LOGN, LR_REQ, IL, p + 1>(v, t, row, valid, sr, si, io, tw, pre);
+        dit_pass<T, LOGN, LR_REQ, IL, p>(v, t, row, valid, xc, io, tw, pre);
+        dit_from<T, LOGN, LR_REQ, IL, p + 1>(v, t, row, valid, xc, io, tw, pre);
     }
 }
 
 // ---- DIF pass p (executed for p = NPASS-1 .. 0) --------------------------
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL, true> &io,
+                                         const Exch<T, LOGN, LR_REQ> &xc, const GIO<T, IL, true> &io,
                                          const TwCat<T> &tw, const vec2_t<T> *pre)
 {
     using Sh = FusedShape<LOGN, LR_REQ>;
@@ -322,8 +376,7 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 if (f % LX::RPL == G) {
                     v[d] = own[f / LX::RPL];
                 } else {
-                    v[d].x = sr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, NS * f)];
-                    v[d].y = si[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, NS * f)];
+                    v[d] = xc.ld_w(p, e, et, NS * f);
                 }
             }
         });
@@ -340,8 +393,7 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
                 if (valid) io.load(row, e, v[d].x, v[d].y);
                 else { v[d].x = T(0); v[d].y = T(0); }
             } else {
-                v[d].x = sr[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f)];
-                v[d].y = si[ex_wr<T, LOGN, LR, Sh::NT>(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f)];
+                v[d] = xc.ld_w(p, e, et, ((P * u) >> SP) * NS * RP + ((P * u) & (NS - 1)) + NS * f);
             }
         }
     }
@@ -365,8 +417,7 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
                     for (int r = 0; r < RP; ++r) {
                         if (r == G) continue;
                         const int e = j + r * (N / RP);
-                        sr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].x;
-                        si[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].y;
+                        xc.st_r(p - 1, e, t, P * u + r * (N / RP), v[u * RP + r]);
                     }
                 }
             });
@@ -377,8 +428,7 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
 #pragma unroll
             for (int r = 0; r < RP; ++r) {
                 const int e = j + r * (N / RP);
-                sr[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].x;
-                si[ex_rd<T, LOGN, LR, Sh::NT>(p - 1, e, t, P * u + r * (N / RP))] = v[u * RP + r].y;
+                xc.st_r(p - 1, e, t, P * u + r * (N / RP), v[u * RP + r]);
             }
         }
         }
@@ -398,12 +448,12 @@ __device__ __forceinline__ void dif_pass(vec2_t<T> *v, int t, int64_t row, bool 
 
 template <typename T, int LOGN, int LR_REQ, bool IL, int p>
 __device__ __forceinline__ void dif_from(vec2_t<T> *v, int t, int64_t row, bool valid,
-                                         T *sr, T *si, const GIO<T, IL, true> &io, const TwCat<T> &tw,
+                                         const Exch<T, LOGN, LR_REQ> &xc, const GIO<T, IL, true> &io, const TwCat<T> &tw,
                                          const vec2_t<T> *pre)
 {
     if constexpr (p >= 0) {
-        dif_pass<T, LOGN, LR_REQ, IL, p>(v, t, row, valid, sr, si, io, tw, pre);
-        dif_from<T, LOGN, LR_REQ, IL, p - 1>(v, t, row, valid, sr, si, io, tw, pre);
+        dif_pass<T, LOGN, LR_REQ, IL, p>(v, t, row, valid, xc, io, tw, pre);
+        dif_from<T, LOGN, LR_REQ, IL, p - 1>(v, t, row, valid, xc, io, tw, pre);
     }
 }
 
@@ -434,8 +484,13 @@ __device__ __forceinline__ void fused_body(const FusedArgs &a)
         }
     } else {
         vec2_t<T> v[R];
-        T *sr = sbase + sl * SSTR;
-        T *si = sbase + S * SSTR + sl * SSTR;
+        Exch<T, LOGN, LR_REQ> xc;
+        if constexpr (FusedX2<T>::value) {
+            xc.sx = reinterpret_cast<vec2_t<T> *>(smem_raw) + sl * SSTR;
+        } else {
+            xc.sr = sbase + sl * SSTR;
+            xc.si = sbase + S * SSTR + sl * SSTR;
+        }
         // fp32: the base factors of passes >= 1, fetched before any data
         vec2_t<T> pre[Sh::NPASS * R];
         if constexpr (PRE && FactorTw<T>::value) {
@@ -453,10 +508,10 @@ __device__ __forceinline__ void fused_body(const FusedArgs &a)
             }
         }
         if constexpr (DIF)
-            dif_from<T, LOGN, LR_REQ, IL, Sh::NPASS - 1>(v, t, row, valid, sr, si, io, tw,
+            dif_from<T, LOGN, LR_REQ, IL, Sh::NPASS - 1>(v, t, row, valid, xc, io, tw,
                                                          (PRE && FactorTw<T>::value) ? pre : nullptr);
         else
-            dit_from<T, LOGN, LR_REQ, IL, 0>(v, t, row, valid, sr, si, io, tw,
+            dit_from<T, LOGN, LR_REQ, IL, 0>(v, t, row, valid, xc, io, tw,
                                              (PRE && FactorTw<T>::value) ? pre : nullptr);
     }
 }

@@ -9,6 +9,7 @@
 
 #include "sfft_launch.h"
 #include "sfft_tma.cuh"
+#include "sfft_tma_warp.cuh"
 
 namespace sfft {
 
@@ -124,6 +125,54 @@ cudaError_t launch_tma(const TmaLaunch &L, cudaStream_t st)
     return e != cudaSuccess ? e : cudaGetLastError();
 #else
     k<<<(unsigned)grid, Sh::NT, Sh::SMEM, st>>>(m_xr, m_xi, m_yr, m_yi, a);
+    count_launch();
+    return cudaGetLastError();
+#endif
+}
+
+// Warp-per-signal bulk-copy kernel (sfft_tma_warp.cuh), N = 1024, radix 32:
+// one CTA of WARPS independent warps per SM, each warp a persistent worker.
+template <typename T, bool DIF, int WARPS, int HK, bool TM>
+cudaError_t launch_tmaw(const TmaLaunch &L, cudaStream_t st)
+{
+    using Sh = TmaWShape<T, WARPS>;
+    auto k = &sfft_tmaw_kernel<T, DIF, WARPS, HK, TM>;
+    static Residency res;
+    int dev = 0, resident = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if ((e = res.get(k, dev, Sh::NT, Sh::SMEM, &resident)) != cudaSuccess) return e;
+    TmaWArgs a;
+    a.x_re = L.inverse ? L.x_im : L.x_re;
+    a.x_im = L.inverse ? L.x_re : L.x_im;
+    a.y_re = L.inverse ? L.y_im : L.y_re;
+    a.y_im = L.inverse ? L.y_re : L.y_im;
+    a.batch = L.batch;
+    a.in_stride = L.in_stride;
+    a.out_stride = L.out_stride;
+    a.scale = L.scale;
+    a.scale_out = L.inverse;
+    a.tw = L.tw;
+    int64_t grid = resident;
+    const int64_t need = (L.batch + WARPS - 1) / WARPS;
+    if (grid > need) grid = need;
+    if (grid < 1) return cudaErrorInvalidConfiguration;   // batch > 0 here: never silently skip work
+#ifndef SFFT_TMA_NO_PDL
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(Sh::NT);
+    cfg.dynamicSmemBytes = Sh::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, k, a);
+    count_launch();
+    return e != cudaSuccess ? e : cudaGetLastError();
+#else
+    k<<<(unsigned)grid, Sh::NT, Sh::SMEM, st>>>(a);
     count_launch();
     return cudaGetLastError();
 #endif

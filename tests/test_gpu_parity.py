@@ -193,7 +193,7 @@ def test_launches_are_counted(cuda):
 TMA_CASES = [("f32", m, lr) for m, lrs in {5: [3], 6: [3, 2], 7: [3, 4], 8: [3, 4], 9: [3, 4],
                                             10: [4, 3, 5], 11: [4, 3], 12: [4, 3]}.items() for lr in lrs] + \
             [("f64", m, lr) for m, lrs in {4: [2], 5: [3], 6: [3], 7: [3, 4], 8: [3, 4], 9: [3],
-                                            10: [3, 4], 11: [4]}.items() for lr in lrs]
+                                            10: [3, 4, 5], 11: [4]}.items() for lr in lrs]
 
 
 @pytest.mark.parametrize("prefetch", [False, True])
@@ -226,6 +226,31 @@ def test_tma_kernel_many_tiles(cuda, dt, m, lr, algo, prefetch):
                                prefetch_factors=prefetch)
             lr_, li_ = sf.fft_split(xr, xi, plan=ldg, inverse=inverse)
             assert torch.equal(lr_, yr) and torch.equal(li_, yi)
+
+
+@pytest.mark.parametrize("algo", ["dit", "dif"])
+def test_warp_kernel_long_persistent_loop(cuda, algo):
+    # fp64 N = 1024 radix 32 (sfft_tma_warp.cuh): ~40 signals per warp, so
+    # both slots of every warp are refilled many times (in-place exchange in
+    # the slot, bulk-copy refill after the exchange read), ragged tail, row
+    # strides > N on both sides
+    m, b = 10, 148 * 7 * 40 + 5
+    rng = np.random.default_rng(9100)
+    re, im = rand(rng, b, 1 << m, np.float64)
+    pad_in, pad_out = 1024 + 32, 1024 + 64
+    xr = torch.zeros(b, pad_in, dtype=torch.float64, device="cuda:0")
+    xi = torch.zeros_like(xr)
+    xr[:, :1024] = torch.from_numpy(re).cuda()
+    xi[:, :1024] = torch.from_numpy(im).cuda()
+    plan = sf.make_plan(m, algo, dtype=torch.float64, device="cuda:0", radix_log=5, kernel="tma")
+    for inverse in (False, True):
+        yr = torch.full((b, pad_out), 7.0, dtype=torch.float64, device="cuda:0")
+        yi = torch.full_like(yr, 7.0)
+        sf.fft_split(xr[:, :1024], xi[:, :1024], plan=plan, inverse=inverse, out=(yr[:, :1024], yi[:, :1024]))
+        wr, wi = oracle.fft_split_c(re, im, algo, inverse)
+        assert np.array_equal(bits(yr[:, :1024].cpu().numpy()), bits(wr))
+        assert np.array_equal(bits(yi[:, :1024].cpu().numpy()), bits(wi))
+        assert bool((yr[:, 1024:] == 7.0).all()) and bool((yi[:, 1024:] == 7.0).all())
 
 
 def test_tma_falls_back_for_unaligned_rows(cuda):
