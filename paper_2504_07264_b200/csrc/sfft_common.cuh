@@ -166,13 +166,14 @@ struct TwTwoLevel {
 };
 
 // Physical slot of logical element e in shared-memory exchange x (the buffer
-// between register pass x and x+1, DIT numbering), per the planned layout
-// (sfft_layouts.h, tools/plan_layouts.py).
-template <typename T, int LOGN, int LR, int NT>
-__device__ __forceinline__ int ex_phys(int x, int e)
+// between register pass x and x+1, DIT numbering), per a planned layout L
+// (sfft_layouts.h, tools/plan_layouts.py): ExLayout (separate exchange
+// buffer, padding allowed) or ExLayoutIP (in place in a tile slot: XOR or
+// identity only, a bijection on [0, N)).
+template <typename L, int ESZ>
+__device__ __forceinline__ int ex_phys_l(int x, int e)
 {
-    using L = ExLayout<(int)sizeof(T), LOGN, LR, NT>;
-    constexpr int mask = sizeof(T) == 4 ? 31 : 15;
+    constexpr int mask = ESZ == 4 ? 31 : 15;
     const int kind = L::kind(x), a = L::arg(x);
     return kind == 0 ? e
          : kind == 1 ? e + (e >> a)
@@ -181,23 +182,39 @@ __device__ __forceinline__ int ex_phys(int x, int e)
 }
 
 // Exchange slots split as (per-thread part) + (compile-time part) when the
-// planner proved the layout additive on that side (ExLayout::lin bit 0 =
-// Stockham writes, bit 1 = next-pass reads): e = e(t,0,0), ec = e(0,u,k), so
-// the kernel addresses the exchange as one base register plus immediates.
+// planner proved the layout additive on that side (L::lin bit 0 = Stockham
+// writes, bit 1 = next-pass reads): e = e(t,0,0), ec = e(0,u,k), so the
+// kernel addresses the exchange as one base register plus immediates.
+template <typename L, int ESZ>
+__device__ __forceinline__ int ex_wr_l(int x, int e, int et, int ec)
+{
+    if (L::lin(x) & 1) return ex_phys_l<L, ESZ>(x, et) + ex_phys_l<L, ESZ>(x, ec);
+    return ex_phys_l<L, ESZ>(x, e);
+}
+
+template <typename L, int ESZ>
+__device__ __forceinline__ int ex_rd_l(int x, int e, int et, int ec)
+{
+    if (L::lin(x) & 2) return ex_phys_l<L, ESZ>(x, et) + ex_phys_l<L, ESZ>(x, ec);
+    return ex_phys_l<L, ESZ>(x, e);
+}
+
+template <typename T, int LOGN, int LR, int NT>
+__device__ __forceinline__ int ex_phys(int x, int e)
+{
+    return ex_phys_l<ExLayout<(int)sizeof(T), LOGN, LR, NT>, (int)sizeof(T)>(x, e);
+}
+
 template <typename T, int LOGN, int LR, int NT>
 __device__ __forceinline__ int ex_wr(int x, int e, int et, int ec)
 {
-    using L = ExLayout<(int)sizeof(T), LOGN, LR, NT>;
-    if (L::lin(x) & 1) return ex_phys<T, LOGN, LR, NT>(x, et) + ex_phys<T, LOGN, LR, NT>(x, ec);
-    return ex_phys<T, LOGN, LR, NT>(x, e);
+    return ex_wr_l<ExLayout<(int)sizeof(T), LOGN, LR, NT>, (int)sizeof(T)>(x, e, et, ec);
 }
 
 template <typename T, int LOGN, int LR, int NT>
 __device__ __forceinline__ int ex_rd(int x, int e, int et, int ec)
 {
-    using L = ExLayout<(int)sizeof(T), LOGN, LR, NT>;
-    if (L::lin(x) & 2) return ex_phys<T, LOGN, LR, NT>(x, et) + ex_phys<T, LOGN, LR, NT>(x, ec);
-    return ex_phys<T, LOGN, LR, NT>(x, e);
+    return ex_rd_l<ExLayout<(int)sizeof(T), LOGN, LR, NT>, (int)sizeof(T)>(x, e, et, ec);
 }
 
 template <typename T, int LOGN, int LR, int NT>

@@ -163,10 +163,13 @@ def plan(n, lr, esz, nt):
     return result
 
 
-def chain(vals):
-    n = len(vals)
-    while n > 1 and vals[n - 1] == 0:
-        n -= 1
+def chain(vals, n=None):
+    """C conditional chain of vals[0..n) (n = the number of exchanges; the
+    last value also answers every x >= n-1)."""
+    if n is None:
+        n = len(vals)
+        while n > 1 and vals[n - 1] == 0:
+            n -= 1
     expr = str(vals[n - 1])
     for x in range(n - 2, -1, -1):
         expr = f"x == {x} ? {vals[x]} : ({expr})"
@@ -222,9 +225,9 @@ def main():
         lines += [
             f"template <> struct ExLayout<{esz}, {logn}, {lr}, {nt}> {{   // wavefronts/ideal: {costs}",
             "    static constexpr bool planned = true;",
-            f"    __host__ __device__ static constexpr int kind(int x) {{ return {chain(kinds)}; }}",
-            f"    __host__ __device__ static constexpr int arg(int x) {{ return {chain(args)}; }}",
-            f"    __host__ __device__ static constexpr int lin(int x) {{ return {chain(lins)}; }}",
+            f"    __host__ __device__ static constexpr int kind(int x) {{ return {chain(kinds, len(res))}; }}",
+            f"    __host__ __device__ static constexpr int arg(int x) {{ return {chain(args, len(res))}; }}",
+            f"    __host__ __device__ static constexpr int lin(int x) {{ return {chain(lins, len(res))}; }}",
             f"    static constexpr int sstr = {sstr};",
             "};",
         ]
