@@ -527,7 +527,7 @@ def run_ours(args):
     bytes_per_launch = 4 * n * cfg.elem_bytes * b
     achieved = bytes_per_launch / (kern_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic(cfg.name, args.algorithm)
-    kname = {"tma": "sfft_tma_kernel", "ldg": "sfft_fused_kernel", "pass": "sfft_pass_kernel"}[plan.kernel]
+    _, k_lr, kname = plan.exec_kernel(b)
     line = {
         "metric": BASELINE_METRIC,
         "value": value,
@@ -543,7 +543,7 @@ def run_ours(args):
         "data": "synthetic (seeded, BASELINE.json config shapes/distributions; workloads.py)",
         "config": {"workload": cfg.name, "n": n, "batch_per_gpu": b, "global_batch": total_rows,
                    "input_dtype": cfg.dtype, "seed": cfg.seed, "algorithm": args.algorithm,
-                   "radix_log": plan.radix_log,
+                   "radix_log": k_lr,
                    "parallelism": (f"batch split into {world} contiguous row blocks (strong), no collective"
                                    if args.scaling == "strong" or world == 1 else
                                    f"batch-sharded x{world}, B rows per GPU (weak), no collective"),
@@ -557,7 +557,7 @@ def run_ours(args):
         "gflops_census": (census["real_mults"] + census["real_adds"]) * total_rows / (ms / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
-                     "kernel": kname + f"<{cfg.dtype}, log2N={cfg.log2n}>",
+                     "kernel": kname + f"<{cfg.dtype}, log2N={cfg.log2n}, radix=2^{k_lr}>",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "unit_of_work": "launch" if n_launch == 1 else "sweep (one pass-group launch)",
                      "sweeps_per_step": n_sweep,

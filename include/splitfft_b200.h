@@ -102,6 +102,14 @@ int sfft_plan_info(const sfft_plan *plan, int *log2n, int *dtype,
 int sfft_exec_schedule(const sfft_plan *plan, int64_t batch, int interleaved,
                        int *launches, int *sweeps);
 
+/* The kernel exec launches for `batch` aligned planar rows (interleaved != 0:
+ * the interleaved layout): family (SFFT_KERNEL_TMA / _LDG / _PASS), its
+ * log2 register radix, and `warp` = 1 when it is the warp-per-signal
+ * bulk-copy kernel (fp64 N = 1024 radix 32).  kernel=auto plans switch
+ * kernels by batch size.  Introspection for the bench's roofline label. */
+int sfft_exec_kernel(const sfft_plan *plan, int64_t batch, int interleaved,
+                     int *family, int *log2_radix, int *warp);
+
 /* Bytes of device workspace exec needs for `batch` rows (0 for the fused
  * single-kernel path, log2n <= 12). */
 int sfft_workspace_bytes(const sfft_plan *plan, int64_t batch, size_t *bytes);

@@ -34,6 +34,8 @@ SIGNATURES = {
     "sfft_plan_info": (_I, [_P] + [ctypes.POINTER(_I)] * 7),
     "sfft_workspace_bytes": (_I, [_P, _I64, ctypes.POINTER(ctypes.c_size_t)]),
     "sfft_exec_schedule": (_I, [_P, _I64, _I, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    "sfft_exec_kernel": (_I, [_P, _I64, _I, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                             ctypes.POINTER(ctypes.c_int)]),
     "sfft_exec_split": (_I, [_P, _P, _P, _P, _P, _I64, _I64, _I64, _I, _P, _P]),
     "sfft_exec_interleaved": (_I, [_P, _P, _P, _I64, _I64, _I64, _I, _P, _P]),
     "sfft_exec_butterfly_stage": (_I, [_I, _I, _I, _P, _I64, _I64, _I, _P]),

@@ -135,6 +135,8 @@ struct sfft_plan {
     int log2n = 0, dtype = 0, algo = 0, device = 0, lr = 0;
     int kernel = SFFT_KERNEL_AUTO;  // fused-path kernel family
     int lr_tma = -1;                // radix of the TMA kernel (-1: none)
+    int lr_tma_small = -1;          // kernel=auto: TMA radix for batches < small_below
+    int64_t small_below = 0;
     int lr_ldg_il = 0;              // radix of the interleaved LDG kernel
     bool pre = false;               // fp32: fetch pass base factors up front
     // fused path
@@ -329,7 +331,9 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
                              ((size_t)is * esz) % 16 == 0 && ((size_t)os * esz) % 16 == 0 &&
                              batch < (int64_t(1) << 31);
         if (!il && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG && aligned) {
-            TmaLaunchFn tf = tma_launcher(p->dtype, m, p->lr_tma, p->algo == SFFT_DIF, p->pre);
+            // kernel=auto batch-size switch (every kernel is the same arithmetic)
+            const int lr_t = (p->lr_tma_small >= 0 && batch < p->small_below) ? p->lr_tma_small : p->lr_tma;
+            TmaLaunchFn tf = tma_launcher(p->dtype, m, lr_t, p->algo == SFFT_DIF, p->pre);
             if (tf) {
                 TmaLaunch L;
                 L.x_re = x0;
@@ -521,6 +525,15 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
         const bool want_tma = kernel == SFFT_KERNEL_TMA ||
                               (kernel == SFFT_KERNEL_AUTO && (log2_radix > 0 || auto_tma));
         if (want_tma && tma_launcher(dtype, log2n, lr, false, p->pre)) p->lr_tma = lr;
+        if (kernel == SFFT_KERNEL_AUTO && log2_radix <= 0 && p->lr_tma >= 0) {
+            int slr = -1;
+            long long below = 0;
+            auto_small_batch(dtype, log2n, &slr, &below);
+            if (slr >= 0 && tma_launcher(dtype, log2n, slr, false, p->pre)) {
+                p->lr_tma_small = slr;
+                p->small_below = below;
+            }
+        }
         if (kernel == SFFT_KERNEL_TMA && p->lr_tma < 0) {
             delete p;
             return fail(SFFT_EINVAL, "no TMA kernel for log2n=%d radix=2^%d", log2n, lr);
@@ -572,6 +585,28 @@ int sfft_plan_info(const sfft_plan *p, int *log2n, int *dtype, int *algorithm, i
     if (device) *device = p->device;
     if (launches) *launches = p->log2n <= kFusedMaxLog ? 1 : (int)p->groups.size();
     if (log2_radix) *log2_radix = p->lr;
+    return SFFT_OK;
+}
+
+int sfft_exec_kernel(const sfft_plan *p, int64_t batch, int interleaved, int *family, int *log2_radix, int *warp)
+{
+    if (!p) return fail(SFFT_EINVAL, "plan is NULL");
+    if (batch < 0) return fail(SFFT_EINVAL, "batch must be >= 0, got %lld", (long long)batch);
+    int fam, lr, w = 0;
+    if (p->log2n > kFusedMaxLog) {
+        fam = SFFT_KERNEL_PASS;
+        lr = p->lr;
+    } else if (!interleaved && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG) {
+        fam = SFFT_KERNEL_TMA;
+        lr = (p->lr_tma_small >= 0 && batch < p->small_below) ? p->lr_tma_small : p->lr_tma;
+        w = p->dtype == SFFT_F64 && p->log2n == 10 && lr == 5;
+    } else {
+        fam = SFFT_KERNEL_LDG;
+        lr = interleaved ? p->lr_ldg_il : p->lr;
+    }
+    if (family) *family = fam;
+    if (log2_radix) *log2_radix = lr;
+    if (warp) *warp = w;
     return SFFT_OK;
 }
 

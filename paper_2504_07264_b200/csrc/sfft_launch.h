@@ -42,6 +42,7 @@ TmaLaunchFn tma_launcher_f64(int logn, int lr, bool dif, bool pre);
 int tma_default_lr(int dtype, int logn);   // -1: no TMA config for this size
 // kernel=auto pick, 0 <= logn <= 12: family 0 = LDG fused, 1 = TMA
 void auto_choice(int dtype, int logn, int *family, int *lr, bool *pre);
+void auto_small_batch(int dtype, int logn, int *lr, long long *below);
 void count_launch();
 
 }  // namespace sfft

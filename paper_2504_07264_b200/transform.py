@@ -105,6 +105,17 @@ class FftPlan:
                                                ctypes.byref(nl), ctypes.byref(ns)))
         return nl.value, ns.value
 
+    def exec_kernel(self, batch: int = 1, interleaved: bool = False):
+        """(family, log2 radix, kernel name) of the kernel one exec of `batch`
+        aligned planar rows launches (kernel='auto' switches by batch size)."""
+        fam, lr, warp = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        _ffi.check(_ffi.lib.sfft_exec_kernel(self._handle, int(batch), int(bool(interleaved)),
+                                             ctypes.byref(fam), ctypes.byref(lr), ctypes.byref(warp)))
+        family = {_ffi.SFFT_KERNEL_TMA: "tma", _ffi.SFFT_KERNEL_LDG: "ldg", _ffi.SFFT_KERNEL_PASS: "pass"}[fam.value]
+        name = ("sfft_tmaw_kernel" if warp.value else
+                {"tma": "sfft_tma_kernel", "ldg": "sfft_fused_kernel", "pass": "sfft_pass_kernel"}[family])
+        return family, lr.value, name
+
     @property
     def radix_log(self) -> int:
         return self._info()[5]

@@ -253,6 +253,26 @@ def test_warp_kernel_long_persistent_loop(cuda, algo):
         assert bool((yr[:, 1024:] == 7.0).all()) and bool((yi[:, 1024:] == 7.0).all())
 
 
+def test_auto_batch_switch_fp64_n1024(cuda):
+    # kernel=auto switches fp64 N = 1024 between the radix-8 TMA kernel (small
+    # batches) and the warp-per-signal radix-32 kernel (>= 2^17 rows); both
+    # are the reference's arithmetic, so results are bitwise equal either way
+    plan = sf.make_plan(10, "dit", dtype=torch.float64, device="cuda:0")
+    assert plan.exec_kernel(1 << 17) == ("tma", 5, "sfft_tmaw_kernel")
+    assert plan.exec_kernel((1 << 17) - 1) == ("tma", 3, "sfft_tma_kernel")
+    assert plan.exec_kernel(1 << 17, interleaved=True)[0] == "ldg"
+    rng = np.random.default_rng(9200)
+    b = 1 << 17
+    re, im = rand(rng, b, 1024, np.float64)
+    xr, xi = torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda()
+    big_r, big_i = sf.fft_split(xr, xi, plan=plan)
+    small_r, small_i = sf.fft_split(xr[:4096], xi[:4096], plan=plan)
+    assert torch.equal(big_r[:4096], small_r) and torch.equal(big_i[:4096], small_i)
+    wr, wi = oracle.fft_split_c(re[:4096], im[:4096])
+    assert np.array_equal(bits(small_r.cpu().numpy()), bits(wr))
+    assert np.array_equal(bits(small_i.cpu().numpy()), bits(wi))
+
+
 def test_tma_falls_back_for_unaligned_rows(cuda):
     m = 6
     rng = np.random.default_rng(8)
