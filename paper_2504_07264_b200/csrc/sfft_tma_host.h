@@ -132,11 +132,11 @@ cudaError_t launch_tma(const TmaLaunch &L, cudaStream_t st)
 
 // Warp-per-signal bulk-copy kernel (sfft_tma_warp.cuh), N = 1024, radix 32:
 // one CTA of WARPS independent warps per SM, each warp a persistent worker.
-template <typename T, bool DIF, int WARPS, int HK, bool TM>
+template <typename T, bool DIF, int WARPS, int HK, bool TM, bool RING = false, int XS = 1>
 cudaError_t launch_tmaw(const TmaLaunch &L, cudaStream_t st)
 {
-    using Sh = TmaWShape<T, WARPS>;
-    auto k = &sfft_tmaw_kernel<T, DIF, WARPS, HK, TM>;
+    using Sh = TmaWShape<T, WARPS, RING, XS>;
+    auto k = &sfft_tmaw_kernel<T, DIF, WARPS, HK, TM, RING, XS>;
     static Residency res;
     int dev = 0, resident = 0;
     cudaError_t e = cudaGetDevice(&dev);

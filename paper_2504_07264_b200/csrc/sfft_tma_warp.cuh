@@ -7,23 +7,28 @@
 // exchanges + global stores), not HBM, bounded the radix-8 TMA kernel on fp64
 // N = 1024 (ncu: l1tex 81%, 1025 shared wavefronts per signal).
 //
-//   * Each warp is an independent persistent worker with its own two slots
-//     (both planes of one signal each) and mbarriers; lane 0 fills a slot
-//     with two non-tensor bulk copies (cp.async.bulk, one contiguous 8 KiB
-//     row per plane for fp64), so the global reads never use LSU wavefronts
-//     and no CTA-wide barrier couples the warps.
+//   * Each warp is an independent persistent worker; the CTA's warps share
+//     one ring of WARPS + XS slots (both planes of one signal each), signal
+//     i of the CTA in slot i % NSLOT, consumed by warp i % WARPS.  The warp
+//     that releases a slot refills it (lane 0: two non-tensor bulk copies,
+//     cp.async.bulk, one contiguous 8 KiB row per plane for fp64) with
+//     signal i + NSLOT, so global reads never use LSU wavefronts, every
+//     warp's next signal is in flight for about one signal period, and a
+//     warp costs ~1 slot instead of 2: 9 warps per SM (10 slots, 160 KiB)
+//     instead of 7 with two slots each (RING = false), +3-5%.
 //   * The slot is linear: the first pass's reads (lane-contiguous) are
 //     conflict-free without a swizzle.  The exchange is written IN PLACE
 //     into the slot once the first pass has read it (XOR layout
 //     phys = e ^ ((e >> 5) & MASK), conflict-free for the Stockham write
 //     (e = 32 lane + f) and the second pass's read (e = lane + 32 r)), and
-//     the slot is refilled after that read -- so a warp needs only 2 x 16
-//     KiB (fp64) and 7 warps fit one SM.
+//     the slot is released (and refilled) right after that read.
 //   * The last pass stores straight to global memory (coalesced 256-byte
 //     warp stores, streaming).
 //   * Factors of the second pass depend only on the lane (column c = lane):
-//     stages 6..5+HK are loaded once into registers for the whole persistent
-//     loop, the rest per signal from the L1-resident stage-major table.
+//     TM = true (shipped): all 31 parked in tensor memory once, fetched per
+//     stage with tcgen05.ld (TmemFactors64 below); TM = false: stages
+//     6..5+HK held in registers, the rest read per signal from the
+//     L1-resident stage-major table (DIT serialised on those loads: 0.77).
 // Arithmetic is the same dit_stages/dif_stages as every other kernel, so
 // fp64 stays bit-identical to the reference.
 #pragma once
@@ -91,18 +96,26 @@ struct TmemFactors64 {
     }
 };
 
-template <typename T, int WARPS>
+// RING = false: each warp owns two slots.  RING = true: the CTA's warps
+// share one ring of WARPS + XS slots -- CTA-local signal i lives in slot
+// i % NSLOT and is consumed by warp i % WARPS, and the warp that releases a
+// slot refills it with signal i + NSLOT (consumed by the next warp) -- so a
+// warp needs ~1 slot instead of 2 and more warps fit an SM (the limit
+// becomes the register file).
+template <typename T, int WARPS, bool RING = false, int XS = 1>
 struct TmaWShape {
     static constexpr int LOGN = 10, N = 1 << LOGN, LR = 5, R = 32, P = 32;
     static constexpr int PLANE = N * (int)sizeof(T);       // bytes of one plane of one signal
     static constexpr int SLOT = 2 * PLANE;                 // both planes
     static constexpr int STAGES = 2;
+    static constexpr int NSLOT = RING ? WARPS + XS : STAGES * WARPS;
     static constexpr int WARP_BYTES = STAGES * SLOT;
     static constexpr int NT = 32 * WARPS;
-    static constexpr int BAR_OFF = WARPS * WARP_BYTES;
-    static constexpr int TADDR_OFF = BAR_OFF + WARPS * STAGES * 8;   // TMEM base written by tcgen05.alloc
+    static constexpr int BAR_OFF = NSLOT * SLOT;
+    static constexpr int REL_OFF = BAR_OFF + NSLOT * 8;     // RING: last released use of each slot
+    static constexpr int TADDR_OFF = REL_OFF + (NSLOT * 4 + 15) / 16 * 16;   // TMEM base (tcgen05.alloc)
     static constexpr int SMEM = TADDR_OFF + 16;
-    static constexpr int TMEM_COLS = WARPS > 4 ? 256 : 128;
+    static constexpr int TMEM_COLS = WARPS > 8 ? 512 : (WARPS > 4 ? 256 : 128);
     static constexpr int MASK = sizeof(T) == 8 ? 15 : 31;  // slots per 128 bytes - 1
 };
 
@@ -113,19 +126,25 @@ __device__ __forceinline__ int xw_phys(int e)
     return e ^ ((e >> 5) & (sizeof(T) == 8 ? 15 : 31));
 }
 
-template <typename T, bool DIF, int WARPS, int HK, bool TM>
+template <typename T, bool DIF, int WARPS, int HK, bool TM, bool RING = false, int XS = 1>
 __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs a)
 {
-    static_assert(!TM || (sizeof(T) == 8 && WARPS <= 8), "TMEM factors: fp64, <= 8 warps");
-    using Sh = TmaWShape<T, WARPS>;
-    constexpr int N = Sh::N, R = Sh::R, LR = Sh::LR;
+    static_assert(!TM || (sizeof(T) == 8 && WARPS <= 12), "TMEM factors: fp64, <= 12 warps");
+    using Sh = TmaWShape<T, WARPS, RING, XS>;
+    constexpr int N = Sh::N, R = Sh::R, LR = Sh::LR, NSLOT = Sh::NSLOT;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    unsigned char *wbuf = smem + warp * Sh::WARP_BYTES;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + Sh::BAR_OFF) + warp * Sh::STAGES;
+    // per-warp mode: this warp's two slots / barriers; ring mode: all of them
+    unsigned char *wbuf = RING ? smem : smem + warp * Sh::WARP_BYTES;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + Sh::BAR_OFF) + (RING ? 0 : warp * Sh::STAGES);
+    volatile int *rel = reinterpret_cast<volatile int *>(smem + Sh::REL_OFF);
     const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
     const int64_t G = (int64_t)gridDim.x * WARPS;
-    const int64_t nk = gw < a.batch ? (a.batch - 1 - gw) / G + 1 : 0;
+    // ring mode: CTA-local signals i = 0 .. nloc-1 (row blockIdx.x + i * gridDim.x)
+    const int64_t nloc = blockIdx.x < a.batch ? (a.batch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int64_t nk = RING ? (nloc > warp ? (nloc - 1 - warp) / WARPS + 1 : 0)
+                            : (gw < a.batch ? (a.batch - 1 - gw) / G + 1 : 0);
+    auto ring_row = [&](int64_t i) { return (int64_t)blockIdx.x + i * gridDim.x; };
     const T *xr = reinterpret_cast<const T *>(a.x_re);
     const T *xi = reinterpret_cast<const T *>(a.x_im);
     T *yr = reinterpret_cast<T *>(a.y_re);
@@ -140,18 +159,36 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
         bulk_load(dst, xr + row * a.in_stride, Sh::PLANE, bar + st);
         bulk_load(dst + Sh::PLANE, xi + row * a.in_stride, Sh::PLANE, bar + st);
     };
-    if (lane == 0) {
-        for (int s = 0; s < Sh::STAGES; ++s) mbar_init(bar + s, 1);
-        fence_mbar_init();
+    if constexpr (RING) {
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < NSLOT; ++s) {
+                mbar_init(bar + s, 1);
+                rel[s] = -1;
+            }
+            fence_mbar_init();
 #ifndef SFFT_TMA_NO_PDL
-        // dependent launch: every global access of this warp follows this
-        // wait (its loads are issued here, its stores follow their data)
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        if (warp == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+            // dependent launch: every load is issued by this thread or by a
+            // warp after its data arrived; every store follows its data
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
-        for (int s = 0; s < Sh::STAGES && s < nk; ++s) issue(s, gw + s * G);
+            for (int s = 0; s < NSLOT && s < nloc; ++s) issue(s, ring_row(s));
+        }
+        __syncthreads();
+    } else {
+        if (lane == 0) {
+            for (int s = 0; s < Sh::STAGES; ++s) mbar_init(bar + s, 1);
+            fence_mbar_init();
+#ifndef SFFT_TMA_NO_PDL
+            // dependent launch: every global access of this warp follows this
+            // wait (its loads are issued here, its stores follow their data)
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (warp == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+            for (int s = 0; s < Sh::STAGES && s < nk; ++s) issue(s, gw + s * G);
+        }
+        __syncwarp();
     }
-    __syncwarp();
 
     // second-pass factors of stages LR+1 .. LR+HK: the lane's column only
     constexpr int NH = TM ? 0 : (1 << HK) - 1;
@@ -192,11 +229,35 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
     };
 
     for (int64_t k = 0; k < nk; ++k) {
-        const int st = (int)(k & 1);
-        const int64_t row = gw + k * G;
+        // ring: local signal i, slot i % NSLOT, its q-th use
+        const int64_t i = warp + k * WARPS;
+        const int st = RING ? (int)(i % NSLOT) : (int)(k & 1);
+        const int64_t q = RING ? i / NSLOT : k >> 1;
+        const int64_t row = RING ? ring_row(i) : gw + k * G;
         T *pr = reinterpret_cast<T *>(wbuf + st * Sh::SLOT);
         T *pi = reinterpret_cast<T *>(wbuf + st * Sh::SLOT + Sh::PLANE);
-        mbar_wait(bar + st, (uint32_t)((k >> 1) & 1));
+        if constexpr (RING) {
+            // the slot's previous use (another warp's signal i - NSLOT) must
+            // have completed its phase before this warp waits on the next
+            // one -- an mbarrier parity wait cannot tell phase q-1 from q+1
+            if (q > 0)
+                while (rel[st] < (int)(q - 1)) {
+                }
+        }
+        mbar_wait(bar + st, (uint32_t)(q & 1));
+        // release this slot (all lanes' reads of it are done) and refill it
+        auto release = [&]() {
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (RING) {
+                    rel[st] = (int)q;
+                    if (i + NSLOT < nloc) issue(st, ring_row(i + NSLOT));
+                } else {
+                    if (k + Sh::STAGES < nk) issue(st, row + Sh::STAGES * G);
+                }
+            }
+        };
         vec2_t<T> v[R];
         if constexpr (!DIF) {
             // pass 0: stages 1..5 on e = lane + 32 r (linear slot)
@@ -221,9 +282,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
                 v[r].x = pr[x];
                 v[r].y = pi[x];
             }
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0 && k + Sh::STAGES < nk) issue(st, row + Sh::STAGES * G);
+            release();
             __syncwarp();
             // pass 1: stages 6..10, column lane
             if constexpr (TM) dit_stages<T, LR, true, false>(v, LR, lane, tw, nullptr, nullptr, &tf);
@@ -253,9 +312,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
                 v[brev(f, LR)].x = pr[x];
                 v[brev(f, LR)].y = pi[x];
             }
-            fence_async_smem();
-            __syncwarp();
-            if (lane == 0 && k + Sh::STAGES < nk) issue(st, row + Sh::STAGES * G);
+            release();
             __syncwarp();
             // pass 0: stages 5..1
             dif_stages<T, LR, true, false>(v, 0, 0, tw);
