@@ -236,9 +236,35 @@ sfft_pass_kernel(const PassArgs a)
     constexpr int SUB = Sh::SUB, LR = Sh::LR, R = Sh::R, P = Sh::P, TJ = Sh::TJ, NT = Sh::NT,
                   RS = Sh::RS, NPI = Sh::NPI;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // the [e][jl] tile: (re, im) pairs in one array (one 64/128-bit shared
+    // access per complex value), or two planes with -DSFFT_PASS_PLANAR_X
     T *sr = reinterpret_cast<T *>(smem_raw);
     T *si = sr + SUB * RS;
+    vec2_t<T> *sx = reinterpret_cast<vec2_t<T> *>(smem_raw);
     vec2_t<T> *cs = reinterpret_cast<vec2_t<T> *>(si + SUB * RS);   // [L][TJ] column factors
+#ifdef SFFT_PASS_PLANAR_X
+    constexpr bool PAIRX = false;
+#else
+    constexpr bool PAIRX = true;
+#endif
+    auto xld = [&](int i) -> vec2_t<T> {
+        if constexpr (PAIRX) {
+            return sx[i];
+        } else {
+            vec2_t<T> w;
+            w.x = sr[i];
+            w.y = si[i];
+            return w;
+        }
+    };
+    auto xst = [&](int i, vec2_t<T> w) {
+        if constexpr (PAIRX) {
+            sx[i] = w;
+        } else {
+            sr[i] = w.x;
+            si[i] = w.y;
+        }
+    };
 
     const int m = a.m;
     const int S = S0 ? 0 : a.S;
@@ -467,8 +493,7 @@ sfft_pass_kernel(const PassArgs a)
                     }                                                                           \
                 }                                                                               \
                 else {                                                                          \
-                    v[u * RP + r].x = sr[e * RS + jl];                                           \
-                    v[u * RP + r].y = si[e * RS + jl];                                           \
+                    v[u * RP + r] = xld(e * RS + jl);                                        \
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \
@@ -493,8 +518,7 @@ sfft_pass_kernel(const PassArgs a)
                 _Pragma("unroll") for (int f = 0; f < RP; ++f)                                  \
                 {                                                                               \
                     const int e = base + nsp * f;                                               \
-                    sr[e * RS + jl] = v[u * RP + brev(f, KP)].x;                                 \
-                    si[e * RS + jl] = v[u * RP + brev(f, KP)].y;                                 \
+                    xst(e * RS + jl, v[u * RP + brev(f, KP)]);                                    \
                 }                                                                               \
             }                                                                                   \
             __syncthreads();                                                                    \
@@ -531,7 +555,8 @@ sfft_pass_kernel(const PassArgs a)
 #pragma unroll
             for (int kk = 0; kk < R; ++kk) {
                 const int k = tid + kk * NT, jj = k >> L, o = k & (SUB - 1);
-                put_out(oaddr(obase + k), sr[o * RS + jj], si[o * RS + jj]);
+                const vec2_t<T> w = xld(o * RS + jj);
+                put_out(oaddr(obase + k), w.x, w.y);
             }
         }
     } else {
@@ -548,8 +573,7 @@ sfft_pass_kernel(const PassArgs a)
 #pragma unroll
             for (int kk = 0; kk < R; ++kk) {
                 const int k = tid + kk * NT, jj = k >> L, o = k & (SUB - 1);
-                sr[o * RS + jj] = v[kk].x;
-                si[o * RS + jj] = v[kk].y;
+                xst(o * RS + jj, v[kk]);
             }
             __syncthreads();
         }
@@ -581,8 +605,7 @@ sfft_pass_kernel(const PassArgs a)
                     }                                                                           \
                 }                                                                               \
                 else {                                                                          \
-                    v[d].x = sr[e * RS + jl];                                                    \
-                    v[d].y = si[e * RS + jl];                                                    \
+                    v[d] = xld(e * RS + jl);                                                    \
                 }                                                                               \
             }                                                                                   \
         }                                                                                       \
@@ -604,8 +627,7 @@ sfft_pass_kernel(const PassArgs a)
                 _Pragma("unroll") for (int r = 0; r < RP; ++r)                                  \
                 {                                                                               \
                     const int e = jp + r * (SUB / RP);                                          \
-                    sr[e * RS + jl] = v[u * RP + r].x;                                           \
-                    si[e * RS + jl] = v[u * RP + r].y;                                           \
+                    xst(e * RS + jl, v[u * RP + r]);                                            \
                 }                                                                               \
             }                                                                                   \
             __syncthreads();                                                                    \

@@ -14,7 +14,7 @@
 //     cp.async.bulk, one contiguous 8 KiB row per plane for fp64) with
 //     signal i + NSLOT, so global reads never use LSU wavefronts, every
 //     warp's next signal is in flight for about one signal period, and a
-//     warp costs ~1 slot instead of 2: 9 warps per SM (10 slots, 160 KiB)
+//     warp costs ~1 slot instead of 2: 9 warps per SM (11 slots, 176 KiB)
 //     instead of 7 with two slots each (RING = false), +3-5%.
 //   * The slot is linear: the first pass's reads (lane-contiguous) are
 //     conflict-free without a swizzle.  The exchange is written IN PLACE

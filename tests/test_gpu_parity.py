@@ -253,16 +253,33 @@ def test_warp_kernel_long_persistent_loop(cuda, algo):
         assert bool((yr[:, 1024:] == 7.0).all()) and bool((yi[:, 1024:] == 7.0).all())
 
 
+@pytest.mark.parametrize("b", [1, 5, 9, 10, 11, 148 * 9 + 1, 148 * 10 * 3 + 7])
+def test_warp_kernel_small_and_ragged_batches(cuda, b):
+    # the slot ring with fewer signals than slots / warps, partial last
+    # rounds and idle warps (they still meet the CTA's final barrier)
+    rng = np.random.default_rng(9300 + b)
+    re, im = rand(rng, b, 1024, np.float64)
+    xr, xi = torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda()
+    for algo in ("dit", "dif"):
+        plan = sf.make_plan(10, algo, dtype=torch.float64, device="cuda:0", radix_log=5, kernel="tma")
+        assert plan.exec_kernel(b)[2] == "sfft_tmaw_kernel"
+        for inverse in (False, True):
+            yr, yi = sf.fft_split(xr, xi, plan=plan, inverse=inverse)
+            wr, wi = oracle.fft_split_c(re, im, algo, inverse)
+            assert np.array_equal(bits(yr.cpu().numpy()), bits(wr))
+            assert np.array_equal(bits(yi.cpu().numpy()), bits(wi))
+
+
 def test_auto_batch_switch_fp64_n1024(cuda):
     # kernel=auto switches fp64 N = 1024 between the radix-8 TMA kernel (small
-    # batches) and the warp-per-signal radix-32 kernel (>= 2^17 rows); both
+    # batches) and the warp-per-signal radix-32 kernel (>= 2^16 rows); both
     # are the reference's arithmetic, so results are bitwise equal either way
     plan = sf.make_plan(10, "dit", dtype=torch.float64, device="cuda:0")
-    assert plan.exec_kernel(1 << 17) == ("tma", 5, "sfft_tmaw_kernel")
-    assert plan.exec_kernel((1 << 17) - 1) == ("tma", 3, "sfft_tma_kernel")
-    assert plan.exec_kernel(1 << 17, interleaved=True)[0] == "ldg"
+    assert plan.exec_kernel(1 << 16) == ("tma", 5, "sfft_tmaw_kernel")
+    assert plan.exec_kernel((1 << 16) - 1) == ("tma", 3, "sfft_tma_kernel")
+    assert plan.exec_kernel(1 << 16, interleaved=True)[0] == "ldg"
     rng = np.random.default_rng(9200)
-    b = 1 << 17
+    b = 1 << 16
     re, im = rand(rng, b, 1024, np.float64)
     xr, xi = torch.from_numpy(re).cuda(), torch.from_numpy(im).cuda()
     big_r, big_i = sf.fft_split(xr, xi, plan=plan)
