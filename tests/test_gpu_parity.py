@@ -191,7 +191,7 @@ def test_launches_are_counted(cuda):
 # ---- the TMA-fed persistent kernel vs the LDG kernel vs the oracle -----------
 
 TMA_CASES = [("f32", m, lr) for m, lrs in {5: [3], 6: [3, 2], 7: [3, 4], 8: [3, 4], 9: [3, 4],
-                                            10: [4, 3, 5], 11: [4, 3], 12: [4, 3]}.items() for lr in lrs] + \
+                                            10: [4, 3, 5], 11: [4, 3], 12: [4, 3, 6]}.items() for lr in lrs] + \
             [("f64", m, lr) for m, lrs in {4: [2], 5: [3], 6: [3], 7: [3, 4], 8: [3, 4], 9: [3],
                                             10: [3, 4, 5], 11: [4]}.items() for lr in lrs]
 
@@ -221,7 +221,10 @@ def test_tma_kernel_many_tiles(cuda, dt, m, lr, algo, prefetch):
             assert np.array_equal(bits(gr), bits(wr)) and np.array_equal(bits(gi), bits(wi))
         else:
             assert rel_l2(gr.astype(np.float64), gi.astype(np.float64), wr, wi) <= F32_TOL(m)
-            # and bit-identical to the LDG kernel (same arithmetic, other data path)
+            # and bit-identical to the LDG kernel (same arithmetic, other data
+            # path); radix 64 (the signal-group kernel) has no LDG twin
+            if lr > 5:
+                continue
             ldg = sf.make_plan(m, algo, dtype=tdt, device="cuda:0", radix_log=lr, kernel="ldg",
                                prefetch_factors=prefetch)
             lr_, li_ = sf.fft_split(xr, xi, plan=ldg, inverse=inverse)
