@@ -21,11 +21,12 @@ DEFAULT_LR = {
 # ("tma" | "ldg", log2 radix, fetch base factors up front (fp32 only)
 #  [, (TMA log2 radix below, batch) -- a batch-size switch: fp64 N = 1024's
 #  warp-per-signal kernel (radix 32) wins from 2^16 rows, the radix-8 TMA
-#  kernel below (fixed per-launch costs; profiles/r02q_f64_n1024_batch_sweep_ring.txt)])
+#  kernel below (fixed per-launch costs; profiles/r02q_f64_n1024_batch_sweep_ring.txt);
+#  radix 0 = the LDG kernel at its default radix])
 AUTO = {
     "f32": {4: ("ldg", 2, False), 5: ("tma", 3, False), 6: ("tma", 3, False), 7: ("tma", 4, False),
             8: ("ldg", 3, False), 9: ("ldg", 3, False), 10: ("ldg", 5, False), 11: ("ldg", 4, False),
-            12: ("ldg", 4, False)},
+            12: ("tma", 6, False, (0, 1 << 13))},
     "f64": {4: ("tma", 2, False), 5: ("ldg", 2, False), 6: ("ldg", 2, False), 7: ("ldg", 3, False),
             8: ("ldg", 3, False), 9: ("ldg", 3, False), 10: ("tma", 5, False, (3, 1 << 16)), 11: ("ldg", 3, False),
             12: ("ldg", 3, False)},
@@ -73,8 +74,12 @@ TMA_CONFIGS = {
 # selected as the TMA family's radix 2^5 for these sizes.  9 warps sharing a
 # ring of 11 slots (176 KiB): +3-5% over 7 warps with two slots each
 # (profiles/r02p_ab_slot_ring.txt, r02q_ab_ring_depth.txt)
-TMAW_CONFIGS = {"f64": {10: (9, 3, 1, 1, 2)}, "f32": {}}
-_tw = os.environ.get("SFFT_TMAW")          # developer override "dt:logn:warps,hk,tm,ring,xs"
+TMAW_CONFIGS = {"f64": {10: (9, 3, 1, 1, 2, 1)}, "f32": {12: (8, 0, 0, 1, 2, 2)}}
+# fp32 N = 4096: two warps per signal, radix 64, 8 warps / 6 slots per SM,
+# factors formed from per-thread base factors (TMEM factors measured no
+# better for fp32: profiles/r02u_ab_cfg4_group_kernel_tmem.txt); +2% over the
+# LDG radix-16 kernel (profiles/r02t_*, r02u_*)
+_tw = os.environ.get("SFFT_TMAW")          # developer override "dt:logn:warps,hk,tm,ring,xs,wps"
 if _tw:
     _dt, _m, _cfg = _tw.split(":")
     TMAW_CONFIGS[_dt][int(_m)] = tuple(int(v) for v in _cfg.split(","))
@@ -213,11 +218,12 @@ def tma_unit(dt):
         f"TmaLaunchFn tma_launcher_{dt}(int logn, int lr, bool dif, bool pre)",
         "{",
     ]
-    for logn, (warps, hk, tm, ring, xs) in sorted(TMAW_CONFIGS[dt].items()):
+    for logn, (warps, hk, tm, ring, xs, wps) in sorted(TMAW_CONFIGS[dt].items()):
         tm = "true" if tm else "false"
         ring = "true" if ring else "false"
-        out.append(f"    if (logn == {logn} && lr == 5) return dif ? launch_tmaw<{T}, true, {warps}, {hk}, {tm}, {ring}, {xs}> "
-                   f": launch_tmaw<{T}, false, {warps}, {hk}, {tm}, {ring}, {xs}>;")
+        a = f"{warps}, {hk}, {tm}, {ring}, {xs}, {logn}, {wps}"
+        out.append(f"    if (logn == {logn} && lr == {logn // 2}) return dif ? launch_tmaw<{T}, true, {a}> "
+                   f": launch_tmaw<{T}, false, {a}>;")
     for logn, cfgs in sorted(TMA_CONFIGS[dt].items()):
         for c in cfgs:
             lr, nt, stages, ob = c[:4]
@@ -305,7 +311,7 @@ def registry_unit():
 
 
 def small_tw_unit():
-    """Stage-t factors (t <= 5) as literals: w_{2^t}^f = cos - j sin of
+    """Stage-t factors (t <= 6) as literals: w_{2^t}^f = cos - j sin of
     2 pi f / 2^t, snapped exactly like twiddle.py:46-57 (Python's math.cos /
     math.sin are libm, bit-identical to the library's host tables).  The
     first register pass of every kernel uses them as immediates, and fp32
@@ -313,7 +319,7 @@ def small_tw_unit():
     import math
     import struct
     re64, im64 = [], []
-    for t in range(1, 6):
+    for t in range(1, 7):
         for f in range(1 << (t - 1)):
             ang = 2.0 * math.pi * f / float(1 << t)
             c, sn = math.cos(ang), math.sin(ang)
@@ -332,7 +338,7 @@ def small_tw_unit():
     d = lambda v: repr(float(v))                                   # noqa: E731
     fl = lambda v: repr(f32(v)) + "f" if f32(v) != int(f32(v)) or abs(f32(v)) > 1 else f"{f32(v):.1f}f"  # noqa: E731
     out = [
-        "// GENERATED by gen_inst.py -- small-stage factors as literals (t <= 5)",
+        "// GENERATED by gen_inst.py -- small-stage factors as literals (t <= 6)",
         "#pragma once",
         "namespace sfft {",
         "// index k = 2^(t-1) - 1 + f for stage t, factor f < 2^(t-1)",

@@ -330,9 +330,11 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         const bool aligned = ((uintptr_t)x0 | (uintptr_t)x1 | (uintptr_t)y0 | (uintptr_t)y1) % 16 == 0 &&
                              ((size_t)is * esz) % 16 == 0 && ((size_t)os * esz) % 16 == 0 &&
                              batch < (int64_t(1) << 31);
-        if (!il && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG && aligned) {
-            // kernel=auto batch-size switch (every kernel is the same arithmetic)
-            const int lr_t = (p->lr_tma_small >= 0 && batch < p->small_below) ? p->lr_tma_small : p->lr_tma;
+        // kernel=auto batch-size switch (fp64: every kernel is the same
+        // arithmetic, bitwise; fp32: within the same tolerance)
+        const bool small = p->lr_tma_small >= 0 && batch < p->small_below;
+        if (!il && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG && aligned && !(small && p->lr_tma_small == 0)) {
+            const int lr_t = small ? p->lr_tma_small : p->lr_tma;
             TmaLaunchFn tf = tma_launcher(p->dtype, m, lr_t, p->algo == SFFT_DIF, p->pre);
             if (tf) {
                 TmaLaunch L;
@@ -516,20 +518,27 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
         else lr = fused_default_lr(dtype, log2n);
         if (log2n == 0) lr = 0;
         if (lr > log2n) lr = log2n;
-        if (lr < 0 || !fused_launcher_algo(dtype, log2n, lr, algorithm == SFFT_DIF, false)) {
+        const bool want_tma_ = kernel == SFFT_KERNEL_TMA ||
+                               (kernel == SFFT_KERNEL_AUTO && (log2_radix > 0 || auto_tma));
+        // a radix may exist for the TMA family only (the fp32 N = 4096
+        // signal-group kernel's radix 64): the LDG kernel (unaligned rows,
+        // interleaved layout) then runs its default radix
+        const bool ldg_ok = lr >= 0 && fused_launcher_algo(dtype, log2n, lr, algorithm == SFFT_DIF, false);
+        const bool tma_only = lr >= 0 && !ldg_ok && want_tma_ && tma_launcher(dtype, log2n, lr, false, false);
+        if (!ldg_ok && !tma_only) {
             delete p;
             return fail(SFFT_EINVAL, "radix 2^%d is not available for log2n=%d", lr, log2n);
         }
-        p->lr = lr;
+        p->lr = ldg_ok ? lr : fused_default_lr(dtype, log2n);
         p->lr_ldg_il = fused_default_lr(dtype, log2n);
-        const bool want_tma = kernel == SFFT_KERNEL_TMA ||
-                              (kernel == SFFT_KERNEL_AUTO && (log2_radix > 0 || auto_tma));
+        const bool want_tma = want_tma_;
         if (want_tma && tma_launcher(dtype, log2n, lr, false, p->pre)) p->lr_tma = lr;
         if (kernel == SFFT_KERNEL_AUTO && log2_radix <= 0 && p->lr_tma >= 0) {
             int slr = -1;
             long long below = 0;
             auto_small_batch(dtype, log2n, &slr, &below);
-            if (slr >= 0 && tma_launcher(dtype, log2n, slr, false, p->pre)) {
+            // slr == 0: the LDG kernel below `below` rows
+            if (slr == 0 || (slr > 0 && tma_launcher(dtype, log2n, slr, false, p->pre))) {
                 p->lr_tma_small = slr;
                 p->small_below = below;
             }
@@ -596,10 +605,12 @@ int sfft_exec_kernel(const sfft_plan *p, int64_t batch, int interleaved, int *fa
     if (p->log2n > kFusedMaxLog) {
         fam = SFFT_KERNEL_PASS;
         lr = p->lr;
-    } else if (!interleaved && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG) {
+    } else if (!interleaved && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG &&
+               !(p->lr_tma_small == 0 && batch < p->small_below)) {
         fam = SFFT_KERNEL_TMA;
         lr = (p->lr_tma_small >= 0 && batch < p->small_below) ? p->lr_tma_small : p->lr_tma;
-        w = p->dtype == SFFT_F64 && p->log2n == 10 && lr == 5;
+        // the signal-group ring kernel (sfft_tma_warp.cuh): radix 2^(log2n/2)
+        w = (p->dtype == SFFT_F64 && p->log2n == 10 && lr == 5) || (p->dtype == SFFT_F32 && p->log2n == 12 && lr == 6);
     } else {
         fam = SFFT_KERNEL_LDG;
         lr = interleaved ? p->lr_ldg_il : p->lr;

@@ -362,6 +362,112 @@ struct NoFP {
     __device__ __forceinline__ void fetch(int, V *) const {}
 };
 
+// One stage of dit with the stage index a template constant (radix
+// 64, K >= 6: the runtime-indexed loop form does not unroll early enough for
+// v[] to stay in registers).
+template <typename T, int K, int t, bool TRIV, bool PACK, int HK, typename TW, typename FP>
+__device__ __forceinline__ void dit_stage_ct(vec2_t<T> *v, int gs, typename TW::index_t cbase, const TW &tw,
+                                              const vec2_t<T> *pre, const vec2_t<T> *hw, const FP *fp)
+{
+    constexpr bool HAS_FP = !std::is_same<FP, NoFP>::value;
+    const bool first = TRIV && gs == 0;
+
+        const int half = (1 << K) >> t;
+        const int i = gs + t;
+        vec2_t<T> wf[HAS_FP ? (1 << (K - 1)) : 1];
+        if constexpr (HAS_FP) {
+            if (!first) fp->fetch(t, wf);
+        }
+        vec2_t<T> base;
+        if (!first && FactorTw<T>::value && !HAS_FP) base = pre ? pre[t - 1] : tw.get(i, cbase);
+#pragma unroll
+        for (int f = 0; f < (1 << (t - 1)); ++f) {
+            const int rf = brev(f, t - 1) * 2 * half;
+            // 0: stage 1 (no factor), 1: identity, 2: quarter turn, 3: generic
+            const int kind = !TRIV ? 3
+                           : i == 1 ? 0
+                           : (SkipTrivial<T>::value && first && f == 0) ? 1
+                           : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
+            vec2_t<T> w, wq;
+            if (kind == 3) {
+                if constexpr (HAS_FP) {
+                    w = first ? stage_factor<T>(t, f, i, first, cbase, gs, tw, base) : wf[f];
+                } else {
+                    w = (hw && !first && t <= HK) ? hw[(1 << (t - 1)) - 1 + f]
+                                                  : stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                }
+                wq = wquad<T>(w);
+            }
+#pragma unroll
+            for (int r = 0; r < half; ++r) {
+                const int p1 = r + rf, p2 = p1 + half;
+                vec2_t<T> tt;
+                if (kind == 3) {
+                    tt = vmul<PACK>(v[p2], w, wq);
+                } else if (kind == 2) {
+                    tt.x = v[p2].y;
+                    tt.y = -v[p2].x;
+                } else {
+                    tt = v[p2];
+                }
+                v[p2] = vsub<PACK>(v[p1], tt);
+                v[p1] = vadd<PACK>(v[p1], tt);
+            }
+        }
+    }
+
+// One stage of dif with the stage index a template constant (radix
+// 64, K >= 6: the runtime-indexed loop form does not unroll early enough for
+// v[] to stay in registers).
+template <typename T, int K, int t, bool TRIV, bool PACK, int HK, typename TW, typename FP>
+__device__ __forceinline__ void dif_stage_ct(vec2_t<T> *v, int gs, typename TW::index_t cbase, const TW &tw,
+                                              const vec2_t<T> *pre, const vec2_t<T> *hw, const FP *fp)
+{
+    constexpr bool HAS_FP = !std::is_same<FP, NoFP>::value;
+    const bool first = TRIV && gs == 0;
+
+        const int half = (1 << K) >> t;
+        const int i = gs + t;
+        vec2_t<T> wf[HAS_FP ? (1 << (K - 1)) : 1];
+        if constexpr (HAS_FP) {
+            if (!first) fp->fetch(t, wf);
+        }
+        vec2_t<T> base;
+        if (!first && FactorTw<T>::value && !HAS_FP) base = pre ? pre[t - 1] : tw.get(i, cbase);
+#pragma unroll
+        for (int f = 0; f < (1 << (t - 1)); ++f) {
+            const int rf = brev(f, t - 1) * 2 * half;
+            const int kind = !TRIV ? 3
+                           : i == 1 ? 0
+                           : (SkipTrivial<T>::value && first && f == 0) ? 1
+                           : (SkipTrivial<T>::value && first && (f << 2) == (1 << t)) ? 2 : 3;
+            vec2_t<T> w, wq;
+            if (kind == 3) {
+                if constexpr (HAS_FP) {
+                    w = first ? stage_factor<T>(t, f, i, first, cbase, gs, tw, base) : wf[f];
+                } else {
+                    w = (hw && !first && t <= HK) ? hw[(1 << (t - 1)) - 1 + f]
+                                                  : stage_factor<T>(t, f, i, first, cbase, gs, tw, base);
+                }
+                wq = wquad<T>(w);
+            }
+#pragma unroll
+            for (int r = 0; r < half; ++r) {
+                const int p1 = r + rf, p2 = p1 + half;
+                const vec2_t<T> d = vsub<PACK>(v[p1], v[p2]);
+                v[p1] = vadd<PACK>(v[p1], v[p2]);
+                if (kind == 3) {
+                    v[p2] = vmul<PACK>(d, w, wq);
+                } else if (kind == 2) {
+                    v[p2].x = d.y;
+                    v[p2].y = -d.x;
+                } else {
+                    v[p2] = d;
+                }
+            }
+        }
+    }
+
 // K consecutive DIT stages (global stages gs+1 .. gs+K) on the 2^K complex
 // values v[0..2^K) (re, im) of one virtual thread.  Register position p
 // holds, before stage t, the (size 2^(gs+t-1)) partial transform of
@@ -388,6 +494,12 @@ __device__ __forceinline__ void dit_stages(vec2_t<T> *v, int gs, typename TW::in
 {
     constexpr bool HAS_FP = !std::is_same<FP, NoFP>::value;
     const bool first = TRIV && gs == 0;   // first pass: every factor is a compile-time constant
+    if constexpr (K >= 6) {
+        static_for<1, K + 1>([&](auto TC) {
+            dit_stage_ct<T, K, decltype(TC)::value, TRIV, PACK, HK>(v, gs, cbase, tw, pre, hw, fp);
+        });
+        return;
+    }
 #pragma unroll
     for (int t = 1; t <= K; ++t) {
         const int half = (1 << K) >> t;
@@ -397,7 +509,7 @@ __device__ __forceinline__ void dit_stages(vec2_t<T> *v, int gs, typename TW::in
             if (!first) fp->fetch(t, wf);
         }
         vec2_t<T> base;
-        if (!first && FactorTw<T>::value) base = pre ? pre[t - 1] : tw.get(i, cbase);
+        if (!first && FactorTw<T>::value && !HAS_FP) base = pre ? pre[t - 1] : tw.get(i, cbase);
 #pragma unroll
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;
@@ -444,6 +556,12 @@ __device__ __forceinline__ void dif_stages(vec2_t<T> *v, int gs, typename TW::in
 {
     constexpr bool HAS_FP = !std::is_same<FP, NoFP>::value;
     const bool first = TRIV && gs == 0;
+    if constexpr (K >= 6) {
+        static_for<0, K>([&](auto IC) {
+            dif_stage_ct<T, K, K - decltype(IC)::value, TRIV, PACK, HK>(v, gs, cbase, tw, pre, hw, fp);
+        });
+        return;
+    }
 #pragma unroll
     for (int t = K; t >= 1; --t) {
         const int half = (1 << K) >> t;
@@ -453,7 +571,7 @@ __device__ __forceinline__ void dif_stages(vec2_t<T> *v, int gs, typename TW::in
             if (!first) fp->fetch(t, wf);
         }
         vec2_t<T> base;
-        if (!first && FactorTw<T>::value) base = pre ? pre[t - 1] : tw.get(i, cbase);
+        if (!first && FactorTw<T>::value && !HAS_FP) base = pre ? pre[t - 1] : tw.get(i, cbase);
 #pragma unroll
         for (int f = 0; f < (1 << (t - 1)); ++f) {
             const int rf = brev(f, t - 1) * 2 * half;

@@ -130,13 +130,14 @@ cudaError_t launch_tma(const TmaLaunch &L, cudaStream_t st)
 #endif
 }
 
-// Warp-per-signal bulk-copy kernel (sfft_tma_warp.cuh), N = 1024, radix 32:
-// one CTA of WARPS independent warps per SM, each warp a persistent worker.
-template <typename T, bool DIF, int WARPS, int HK, bool TM, bool RING = false, int XS = 1>
+// Signal-group bulk-copy kernel (sfft_tma_warp.cuh): one CTA of WARPS warps
+// per SM, WPS warps per signal, each group a persistent worker.
+template <typename T, bool DIF, int WARPS, int HK, bool TM, bool RING = false, int XS = 1, int LOGN = 10,
+          int WPS = 1>
 cudaError_t launch_tmaw(const TmaLaunch &L, cudaStream_t st)
 {
-    using Sh = TmaWShape<T, WARPS, RING, XS>;
-    auto k = &sfft_tmaw_kernel<T, DIF, WARPS, HK, TM, RING, XS>;
+    using Sh = TmaWShape<T, WARPS, RING, XS, LOGN, WPS>;
+    auto k = &sfft_tmaw_kernel<T, DIF, WARPS, HK, TM, RING, XS, LOGN, WPS>;
     static Residency res;
     int dev = 0, resident = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -154,7 +155,7 @@ cudaError_t launch_tmaw(const TmaLaunch &L, cudaStream_t st)
     a.scale_out = L.inverse;
     a.tw = L.tw;
     int64_t grid = resident;
-    const int64_t need = (L.batch + WARPS - 1) / WARPS;
+    const int64_t need = (L.batch + Sh::GROUPS - 1) / Sh::GROUPS;
     if (grid > need) grid = need;
     if (grid < 1) return cudaErrorInvalidConfiguration;   // batch > 0 here: never silently skip work
 #ifndef SFFT_TMA_NO_PDL

@@ -26,7 +26,7 @@
 //     warp stores, streaming).
 //   * Factors of the second pass depend only on the lane (column c = lane):
 //     TM = true (shipped): all 31 parked in tensor memory once, fetched per
-//     stage with tcgen05.ld (TmemFactors64 below); TM = false: stages
+//     stage with tcgen05.ld (TmemFactors below); TM = false: stages
 //     6..5+HK held in registers, the rest read per signal from the
 //     L1-resident stage-major table (DIT serialised on those loads: 0.77).
 // Arithmetic is the same dit_stages/dif_stages as every other kernel, so
@@ -62,53 +62,83 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 // register file keeps only the current stage's factors, where L1 loads of
 // the whole set either spilled (all 31 factors hoisted: 124 registers next
 // to the 128 of the data) or serialised on their latency.
-struct TmemFactors64 {
+template <typename T>
+struct TmemFactors {
+    static constexpr int W = 2 * (int)sizeof(T) / 4;   // 32-bit columns per complex factor
     uint32_t taddr;            // lane quarter << 16 | column block
-    __device__ __forceinline__ void fetch(int t, double2 *w) const
+    __device__ __forceinline__ void fetch(int t, vec2_t<T> *w) const
     {
         const int n = 1 << (t - 1), i0 = n - 1;
-        uint32_t r[16][4];
+        uint32_t r[32][4];
         // constant trip counts (guarded) so the loops unroll before t is known
 #pragma unroll
-        for (int f = 0; f < 16; ++f)
-            if (f < n)
-                asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(r[f][0]), "=r"(r[f][1]), "=r"(r[f][2]), "=r"(r[f][3])
-                         : "r"(taddr + 4 * (i0 + f)));
+        for (int f = 0; f < 32; ++f) {
+            if (f < n) {
+                if constexpr (W == 4)
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(r[f][0]), "=r"(r[f][1]), "=r"(r[f][2]), "=r"(r[f][3])
+                                 : "r"(taddr + W * (i0 + f)));
+                else
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+                                 : "=r"(r[f][0]), "=r"(r[f][1])
+                                 : "r"(taddr + W * (i0 + f)));
+            }
+        }
 #pragma unroll
-        for (int f = 0; f < 16; ++f) {
+        for (int f = 0; f < 32; ++f) {
             if (f >= n) break;
             // the wait names the registers it makes valid, so no use is
             // scheduled above it (only the first one actually waits)
-            asm volatile("tcgen05.wait::ld.sync.aligned;"
-                         : "+r"(r[f][0]), "+r"(r[f][1]), "+r"(r[f][2]), "+r"(r[f][3]));
-            w[f] = make_double2(__hiloint2double((int)r[f][1], (int)r[f][0]),
-                                __hiloint2double((int)r[f][3], (int)r[f][2]));
+            if constexpr (W == 4) {
+                asm volatile("tcgen05.wait::ld.sync.aligned;"
+                             : "+r"(r[f][0]), "+r"(r[f][1]), "+r"(r[f][2]), "+r"(r[f][3]));
+                w[f] = make_double2(__hiloint2double((int)r[f][1], (int)r[f][0]),
+                                    __hiloint2double((int)r[f][3], (int)r[f][2]));
+            } else {
+                asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[f][0]), "+r"(r[f][1]));
+                vec2_t<T> x;
+                x.x = __uint_as_float(r[f][0]);
+                x.y = __uint_as_float(r[f][1]);
+                w[f] = x;
+            }
         }
     }
-    __device__ __forceinline__ void put(int i, double2 w) const
+    __device__ __forceinline__ void put(int i, vec2_t<T> w) const
     {
-        const uint32_t lo0 = (uint32_t)__double2loint(w.x), hi0 = (uint32_t)__double2hiint(w.x);
-        const uint32_t lo1 = (uint32_t)__double2loint(w.y), hi1 = (uint32_t)__double2hiint(w.y);
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + 4 * i), "r"(lo0),
-                     "r"(hi0), "r"(lo1), "r"(hi1)
-                     : "memory");
+        if constexpr (W == 4) {
+            const uint32_t lo0 = (uint32_t)__double2loint(w.x), hi0 = (uint32_t)__double2hiint(w.x);
+            const uint32_t lo1 = (uint32_t)__double2loint(w.y), hi1 = (uint32_t)__double2hiint(w.y);
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr + W * i),
+                         "r"(lo0), "r"(hi0), "r"(lo1), "r"(hi1)
+                         : "memory");
+        } else {
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(taddr + W * i),
+                         "r"(__float_as_uint(w.x)), "r"(__float_as_uint(w.y))
+                         : "memory");
+        }
     }
 };
 
-// RING = false: each warp owns two slots.  RING = true: the CTA's warps
-// share one ring of WARPS + XS slots -- CTA-local signal i lives in slot
-// i % NSLOT and is consumed by warp i % WARPS, and the warp that releases a
-// slot refills it with signal i + NSLOT (consumed by the next warp) -- so a
-// warp needs ~1 slot instead of 2 and more warps fit an SM (the limit
-// becomes the register file).
-template <typename T, int WARPS, bool RING = false, int XS = 1>
+// RING = false: each warp owns two slots.  RING = true: the CTA's signal
+// groups share one ring of GROUPS + XS slots -- CTA-local signal i lives in
+// slot i % NSLOT and is consumed by group i % GROUPS, and the group that
+// releases a slot refills it with signal i + NSLOT (consumed by the next
+// group) -- so a group needs ~1 slot instead of 2 and more warps fit an SM
+// (the limit becomes the register file).
+// A signal of N = 2^LOGN points is owned by a group of WPS warps (P = 32 WPS
+// threads x R = N / P values, two register passes of LR = log2 R stages):
+// fp64 N = 1024: one warp, radix 32; fp32 N = 4096: two warps, radix 64.
+template <typename T, int WARPS, bool RING = false, int XS = 1, int LOGN_ = 10, int WPS = 1>
 struct TmaWShape {
-    static constexpr int LOGN = 10, N = 1 << LOGN, LR = 5, R = 32, P = 32;
+    static constexpr int LOGN = LOGN_, N = 1 << LOGN, P = 32 * WPS, R = N / P;
+    static constexpr int LR = LOGN / 2;
+    static_assert((1 << LR) == R && 2 * LR == LOGN, "two register passes of log2(N/P) stages");
+    static_assert(WARPS % WPS == 0, "whole signal groups per CTA");
+    static constexpr int GROUPS = WARPS / WPS;
     static constexpr int PLANE = N * (int)sizeof(T);       // bytes of one plane of one signal
     static constexpr int SLOT = 2 * PLANE;                 // both planes
     static constexpr int STAGES = 2;
-    static constexpr int NSLOT = RING ? WARPS + XS : STAGES * WARPS;
+    static constexpr int NSLOT = RING ? GROUPS + XS : STAGES * WARPS;
     static constexpr int WARP_BYTES = STAGES * SLOT;
     static constexpr int NT = 32 * WARPS;
     static constexpr int BAR_OFF = NSLOT * SLOT;
@@ -116,24 +146,33 @@ struct TmaWShape {
     static constexpr int TADDR_OFF = REL_OFF + (NSLOT * 4 + 15) / 16 * 16;   // TMEM base (tcgen05.alloc)
     static constexpr int SMEM = TADDR_OFF + 16;
     static constexpr int TMEM_COLS = WARPS > 8 ? 512 : (WARPS > 4 ? 256 : 128);
-    static constexpr int MASK = sizeof(T) == 8 ? 15 : 31;  // slots per 128 bytes - 1
 };
 
-// exchange slot of logical element e (see the header comment)
-template <typename T>
+// exchange slot of logical element e, 8-byte elements (fp64 planar values or
+// fp32 (re, im) pairs): XOR of the 16 slots of each 128-byte line with the
+// element's "row" e >> LR -- conflict-free for the Stockham write
+// (e = P t + f) and the next pass's read (e = t + P r) when P = 2^LR.
+template <int LR>
 __device__ __forceinline__ int xw_phys(int e)
 {
-    return e ^ ((e >> 5) & (sizeof(T) == 8 ? 15 : 31));
+    return e ^ ((e >> LR) & 15);
 }
 
-template <typename T, bool DIF, int WARPS, int HK, bool TM, bool RING = false, int XS = 1>
+template <typename T, bool DIF, int WARPS, int HK, bool TM, bool RING = false, int XS = 1, int LOGN_ = 10, int WPS = 1>
 __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs a)
 {
-    static_assert(!TM || (sizeof(T) == 8 && WARPS <= 12), "TMEM factors: fp64, <= 12 warps");
-    using Sh = TmaWShape<T, WARPS, RING, XS>;
-    constexpr int N = Sh::N, R = Sh::R, LR = Sh::LR, NSLOT = Sh::NSLOT;
+    static_assert(!TM || WARPS <= 12, "TMEM factors: <= 3 warps per lane quarter");
+    static_assert(RING || WPS == 1, "groups of several warps use the slot ring");
+    using Sh = TmaWShape<T, WARPS, RING, XS, LOGN_, WPS>;
+    constexpr int N = Sh::N, R = Sh::R, LR = Sh::LR, P = Sh::P, NSLOT = Sh::NSLOT, GROUPS = Sh::GROUPS;
+    // fp32: (re, im) pairs in the exchange, packed f32x2 math, stage factors
+    // formed from per-thread base factors (FactorTw); fp64: planar exchange,
+    // scalar math, table factors (bit-exact contract)
+    constexpr bool F32 = sizeof(T) == 4;
     extern __shared__ __align__(128) unsigned char smem[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int grp = warp / WPS;                       // signal group of this warp
+    const int t = threadIdx.x % P;                    // thread of the signal
     // per-warp mode: this warp's two slots / barriers; ring mode: all of them
     unsigned char *wbuf = RING ? smem : smem + warp * Sh::WARP_BYTES;
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + Sh::BAR_OFF) + (RING ? 0 : warp * Sh::STAGES);
@@ -142,7 +181,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
     const int64_t G = (int64_t)gridDim.x * WARPS;
     // ring mode: CTA-local signals i = 0 .. nloc-1 (row blockIdx.x + i * gridDim.x)
     const int64_t nloc = blockIdx.x < a.batch ? (a.batch - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    const int64_t nk = RING ? (nloc > warp ? (nloc - 1 - warp) / WARPS + 1 : 0)
+    const int64_t nk = RING ? (nloc > grp ? (nloc - 1 - grp) / GROUPS + 1 : 0)
                             : (gw < a.batch ? (a.batch - 1 - gw) / G + 1 : 0);
     auto ring_row = [&](int64_t i) { return (int64_t)blockIdx.x + i * gridDim.x; };
     const T *xr = reinterpret_cast<const T *>(a.x_re);
@@ -152,6 +191,11 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
     const TwCat<T> tw{reinterpret_cast<const vec2_t<T> *>(a.tw)};
     const T scale = (T)a.scale;
     const bool do_scale = a.scale_out != 0;
+    // barrier among the P threads of this signal
+    auto gsync = [&]() {
+        if constexpr (WPS == 1) __syncwarp();
+        else asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(P) : "memory");
+    };
 
     auto issue = [&](int st, int64_t row) {
         mbar_expect_tx(bar + st, Sh::SLOT);
@@ -168,7 +212,7 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
             fence_mbar_init();
 #ifndef SFFT_TMA_NO_PDL
             // dependent launch: every load is issued by this thread or by a
-            // warp after its data arrived; every store follows its data
+            // group after its data arrived; every store follows its data
             asm volatile("griddepcontrol.wait;" ::: "memory");
             asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
@@ -190,15 +234,22 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
         __syncwarp();
     }
 
-    // second-pass factors of stages LR+1 .. LR+HK: the lane's column only
-    constexpr int NH = TM ? 0 : (1 << HK) - 1;
+    // second-pass factors of stages LR+1 .. LR+HK (fp64, TM = false): the
+    // thread's column only
+    constexpr int NH = (TM || F32) ? 0 : (1 << HK) - 1;
     vec2_t<T> hw[NH > 0 ? NH : 1];
 #pragma unroll
-    for (int t = 1; t <= (TM ? 0 : HK); ++t)
+    for (int tt = 1; tt <= ((TM || F32) ? 0 : HK); ++tt)
 #pragma unroll
-        for (int f = 0; f < (1 << (t - 1)); ++f) hw[(1 << (t - 1)) - 1 + f] = tw.get(LR + t, lane + (f << LR));
-    // TM: all 31 second-pass factors in tensor memory instead
-    TmemFactors64 tf;
+        for (int f = 0; f < (1 << (tt - 1)); ++f) hw[(1 << (tt - 1)) - 1 + f] = tw.get(LR + tt, t + (f << LR));
+    // fp32: base factors w_{LR+tt}(t) of the second pass, once for all signals
+    vec2_t<T> pre[F32 ? LR : 1];
+    if constexpr (F32 && !TM) {
+#pragma unroll
+        for (int tt = 1; tt <= LR; ++tt) pre[tt - 1] = tw.get(LR + tt, t);
+    }
+    // TM: all second-pass factors in tensor memory instead
+    TmemFactors<T> tf;
     uint32_t *taddr_sm = reinterpret_cast<uint32_t *>(smem + Sh::TADDR_OFF);
     if constexpr (TM) {
         if (warp == 0) {
@@ -211,11 +262,16 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         tf.taddr = *taddr_sm + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(128 * (warp >> 2));
+        // every second-pass factor of column t, exactly as the stage helpers
+        // form it (fp64: table values; fp32: base x immediate, FactorTw)
 #pragma unroll
-        for (int t = 1; t <= LR; ++t)
+        for (int tt = 1; tt <= LR; ++tt) {
+            vec2_t<T> base{};
+            if constexpr (F32) base = tw.get(LR + tt, t);
 #pragma unroll
-            for (int f = 0; f < (1 << (t - 1)); ++f)
-                tf.put((1 << (t - 1)) - 1 + f, tw.get(LR + t, lane + (f << LR)));
+            for (int f = 0; f < (1 << (tt - 1)); ++f)
+                tf.put((1 << (tt - 1)) - 1 + f, stage_factor<T>(tt, f, LR + tt, false, t, LR, tw, base));
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
 
@@ -227,29 +283,64 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
         st_stream(yr + row * a.out_stride + e, v.x);
         st_stream(yi + row * a.out_stride + e, v.y);
     };
+    // second-pass stages (DIT ascending / DIF descending), column t
+    auto pass1 = [&](vec2_t<T> *v) {
+        if constexpr (TM) {
+            if constexpr (!DIF) dit_stages<T, LR, true, F32>(v, LR, t, tw, nullptr, nullptr, &tf);
+            else dif_stages<T, LR, true, F32>(v, LR, t, tw, nullptr, nullptr, &tf);
+        } else if constexpr (F32) {
+            if constexpr (!DIF) dit_stages<T, LR, true, true>(v, LR, t, tw, pre);
+            else dif_stages<T, LR, true, true>(v, LR, t, tw, pre);
+        } else {
+            if constexpr (!DIF) dit_stages<T, LR, true, false, HK>(v, LR, t, tw, nullptr, hw);
+            else dif_stages<T, LR, true, false, HK>(v, LR, t, tw, nullptr, hw);
+        }
+    };
 
     for (int64_t k = 0; k < nk; ++k) {
         // ring: local signal i, slot i % NSLOT, its q-th use
-        const int64_t i = warp + k * WARPS;
+        const int64_t i = grp + k * GROUPS;
         const int st = RING ? (int)(i % NSLOT) : (int)(k & 1);
         const int64_t q = RING ? i / NSLOT : k >> 1;
         const int64_t row = RING ? ring_row(i) : gw + k * G;
         T *pr = reinterpret_cast<T *>(wbuf + st * Sh::SLOT);
         T *pi = reinterpret_cast<T *>(wbuf + st * Sh::SLOT + Sh::PLANE);
+        vec2_t<T> *px = reinterpret_cast<vec2_t<T> *>(wbuf + st * Sh::SLOT);
+        // exchange access (8-byte elements): fp64 planar, fp32 pairs
+        auto xget = [&](int e) -> vec2_t<T> {
+            const int x = xw_phys<LR>(e);
+            vec2_t<T> w;
+            if constexpr (F32) {
+                w = px[x];
+            } else {
+                w.x = pr[x];
+                w.y = pi[x];
+            }
+            return w;
+        };
+        auto xput = [&](int e, vec2_t<T> w) {
+            const int x = xw_phys<LR>(e);
+            if constexpr (F32) {
+                px[x] = w;
+            } else {
+                pr[x] = w.x;
+                pi[x] = w.y;
+            }
+        };
         if constexpr (RING) {
-            // the slot's previous use (another warp's signal i - NSLOT) must
-            // have completed its phase before this warp waits on the next
+            // the slot's previous use (another group's signal i - NSLOT) must
+            // have completed its phase before this group waits on the next
             // one -- an mbarrier parity wait cannot tell phase q-1 from q+1
             if (q > 0)
                 while (rel[st] < (int)(q - 1)) {
                 }
         }
         mbar_wait(bar + st, (uint32_t)(q & 1));
-        // release this slot (all lanes' reads of it are done) and refill it
+        // release this slot (all reads of it are done) and refill it
         auto release = [&]() {
             fence_async_smem();
-            __syncwarp();
-            if (lane == 0) {
+            gsync();
+            if (t == 0) {
                 if constexpr (RING) {
                     rel[st] = (int)q;
                     if (i + NSLOT < nloc) issue(st, ring_row(i + NSLOT));
@@ -260,64 +351,46 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
         };
         vec2_t<T> v[R];
         if constexpr (!DIF) {
-            // pass 0: stages 1..5 on e = lane + 32 r (linear slot)
+            // pass 0: stages 1..LR on e = t + P r (linear slot)
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                v[r].x = pr[lane + 32 * r];
-                v[r].y = pi[lane + 32 * r];
+                v[r].x = pr[t + P * r];
+                v[r].y = pi[t + P * r];
             }
-            dit_stages<T, LR, true, false>(v, 0, 0, tw);
-            __syncwarp();
-            // Stockham scatter in place: e = 32 lane + f <- register rev(f)
+            dit_stages<T, LR, true, F32>(v, 0, 0, tw);
+            gsync();
+            // Stockham scatter in place: e = P t + f <- register rev(f)
 #pragma unroll
-            for (int f = 0; f < R; ++f) {
-                const int x = xw_phys<T>(32 * lane + f);
-                pr[x] = v[brev(f, LR)].x;
-                pi[x] = v[brev(f, LR)].y;
-            }
-            __syncwarp();
+            for (int f = 0; f < R; ++f) xput(P * t + f, v[brev(f, LR)]);
+            gsync();
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int x = xw_phys<T>(lane + 32 * r);
-                v[r].x = pr[x];
-                v[r].y = pi[x];
-            }
+            for (int r = 0; r < R; ++r) v[r] = xget(t + P * r);
             release();
-            __syncwarp();
-            // pass 1: stages 6..10, column lane
-            if constexpr (TM) dit_stages<T, LR, true, false>(v, LR, lane, tw, nullptr, nullptr, &tf);
-            else dit_stages<T, LR, true, false, HK>(v, LR, lane, tw, nullptr, hw);
+            if constexpr (WPS == 1) __syncwarp();
+            // pass 1: stages LR+1 .. 2 LR, column t
+            pass1(v);
 #pragma unroll
-            for (int f = 0; f < R; ++f) put(row, lane + 32 * f, v[brev(f, LR)]);
+            for (int f = 0; f < R; ++f) put(row, t + P * f, v[brev(f, LR)]);
         } else {
-            // DIF pass 1 (stages 10..6, column lane) reads e = lane + 32 f into register rev(f)
+            // DIF pass 1 (stages 2 LR .. LR+1, column t) reads e = t + P f into register rev(f)
 #pragma unroll
             for (int f = 0; f < R; ++f) {
-                v[brev(f, LR)].x = pr[lane + 32 * f];
-                v[brev(f, LR)].y = pi[lane + 32 * f];
+                v[brev(f, LR)].x = pr[t + P * f];
+                v[brev(f, LR)].y = pi[t + P * f];
             }
-            if constexpr (TM) dif_stages<T, LR, true, false>(v, LR, lane, tw, nullptr, nullptr, &tf);
-            else dif_stages<T, LR, true, false, HK>(v, LR, lane, tw, nullptr, hw);
-            __syncwarp();
+            pass1(v);
+            gsync();
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int x = xw_phys<T>(lane + 32 * r);
-                pr[x] = v[r].x;
-                pi[x] = v[r].y;
-            }
-            __syncwarp();
+            for (int r = 0; r < R; ++r) xput(t + P * r, v[r]);
+            gsync();
 #pragma unroll
-            for (int f = 0; f < R; ++f) {
-                const int x = xw_phys<T>(32 * lane + f);
-                v[brev(f, LR)].x = pr[x];
-                v[brev(f, LR)].y = pi[x];
-            }
+            for (int f = 0; f < R; ++f) v[brev(f, LR)] = xget(P * t + f);
             release();
-            __syncwarp();
-            // pass 0: stages 5..1
-            dif_stages<T, LR, true, false>(v, 0, 0, tw);
+            if constexpr (WPS == 1) __syncwarp();
+            // pass 0: stages LR..1
+            dif_stages<T, LR, true, F32>(v, 0, 0, tw);
 #pragma unroll
-            for (int r = 0; r < R; ++r) put(row, lane + 32 * r, v[r]);
+            for (int r = 0; r < R; ++r) put(row, t + P * r, v[r]);
         }
     }
     if constexpr (TM) {

@@ -281,6 +281,11 @@ def test_auto_batch_switch_fp64_n1024(cuda):
     assert plan.exec_kernel(1 << 16) == ("tma", 5, "sfft_tmaw_kernel")
     assert plan.exec_kernel((1 << 16) - 1) == ("tma", 3, "sfft_tma_kernel")
     assert plan.exec_kernel(1 << 16, interleaved=True)[0] == "ldg"
+    # fp32 N = 4096: the two-warp radix-64 signal-group kernel from 2^13 rows,
+    # the LDG radix-16 kernel below
+    p32 = sf.make_plan(12, "dit", dtype=torch.float32, device="cuda:0")
+    assert p32.exec_kernel(1 << 13) == ("tma", 6, "sfft_tmaw_kernel")
+    assert p32.exec_kernel((1 << 13) - 1)[0] == "ldg"
     rng = np.random.default_rng(9200)
     b = 1 << 16
     re, im = rand(rng, b, 1024, np.float64)
