@@ -79,7 +79,7 @@ TMAW_CONFIGS = {"f64": {10: (9, 3, 1, 1, 2, 1)}, "f32": {12: (8, 0, 0, 1, 2, 2)}
 # factors formed from per-thread base factors (TMEM factors measured no
 # better for fp32: profiles/r02u_ab_cfg4_group_kernel_tmem.txt); +2% over the
 # LDG radix-16 kernel (profiles/r02t_*, r02u_*)
-_tw = os.environ.get("SFFT_TMAW")          # developer override "dt:logn:warps,hk,tm,ring,xs,wps"
+_tw = os.environ.get("SFFT_TMAW")          # developer override "dt:logn:warps,hk,tm,ring,xs,wps[,pf]"
 if _tw:
     _dt, _m, _cfg = _tw.split(":")
     TMAW_CONFIGS[_dt][int(_m)] = tuple(int(v) for v in _cfg.split(","))
@@ -107,6 +107,7 @@ def fused_unit(dt, algo):
     dif = "true" if algo == "dif" else "false"
     out = [
         "// GENERATED by gen_inst.py -- do not edit",
+        "#include <atomic>",
         '#include "sfft_fused.cuh"',
         '#include "sfft_launch.h"',
         "namespace sfft {",
@@ -117,13 +118,15 @@ def fused_unit(dt, algo):
         f"    auto k = fused_kernel_for<{T}, LOGN, LR, {dif}, IL, PRE>();",
         f"    constexpr int smem = Sh::template smem_bytes<{T}>();",
         "    if (smem > 48 * 1024) {",
-        "        static int done_mask = 0;",
+        "        // per-device 'attribute set' bits; concurrent first calls may both set",
+        "        // it (idempotent), none launches before its own call returned",
+        "        static std::atomic<unsigned> done_mask{0u};",
         "        int dev = 0;",
         "        cudaGetDevice(&dev);",
-        "        if (!(done_mask & (1 << (dev & 31)))) {",
+        "        if (!(done_mask.load(std::memory_order_acquire) & (1u << (dev & 31)))) {",
         "            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);",
         "            if (e != cudaSuccess) return e;",
-        "            done_mask |= 1 << (dev & 31);",
+        "            done_mask.fetch_or(1u << (dev & 31), std::memory_order_release);",
         "        }",
         "    }",
         "    const int64_t grid = (a.batch + Sh::S - 1) / Sh::S;",
@@ -169,6 +172,7 @@ def pass_unit(dt):
               (False, False, False, True, True), (False, False, False, False, True)]
     out = [
         "// GENERATED by gen_inst.py -- do not edit",
+        "#include <atomic>",
         '#include "sfft_pass.cuh"',
         '#include "sfft_launch.h"',
         "namespace sfft {",
@@ -179,13 +183,15 @@ def pass_unit(dt):
         f"    auto k = sfft_pass_kernel<{T}, L, {lr}, DIF, ILI, ILO, S0, DIST>;",
         "    constexpr int smem = Sh::smem_bytes();",
         "    if (smem > 48 * 1024) {",
-        "        static int done_mask = 0;",
+        "        // per-device 'attribute set' bits; concurrent first calls may both set",
+        "        // it (idempotent), none launches before its own call returned",
+        "        static std::atomic<unsigned> done_mask{0u};",
         "        int dev = 0;",
         "        cudaGetDevice(&dev);",
-        "        if (!(done_mask & (1 << (dev & 31)))) {",
+        "        if (!(done_mask.load(std::memory_order_acquire) & (1u << (dev & 31)))) {",
         "            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);",
         "            if (e != cudaSuccess) return e;",
-        "            done_mask |= 1 << (dev & 31);",
+        "            done_mask.fetch_or(1u << (dev & 31), std::memory_order_release);",
         "        }",
         "    }",
         "    k<<<(unsigned)grid, Sh::NT, smem, st>>>(a);",
@@ -218,10 +224,12 @@ def tma_unit(dt):
         f"TmaLaunchFn tma_launcher_{dt}(int logn, int lr, bool dif, bool pre)",
         "{",
     ]
-    for logn, (warps, hk, tm, ring, xs, wps) in sorted(TMAW_CONFIGS[dt].items()):
+    for logn, c in sorted(TMAW_CONFIGS[dt].items()):
+        warps, hk, tm, ring, xs, wps = c[:6]
+        pf = c[6] if len(c) > 6 else 0
         tm = "true" if tm else "false"
         ring = "true" if ring else "false"
-        a = f"{warps}, {hk}, {tm}, {ring}, {xs}, {logn}, {wps}"
+        a = f"{warps}, {hk}, {tm}, {ring}, {xs}, {logn}, {wps}, {pf}"
         out.append(f"    if (logn == {logn} && lr == {logn // 2}) return dif ? launch_tmaw<{T}, true, {a}> "
                    f": launch_tmaw<{T}, false, {a}>;")
     for logn, cfgs in sorted(TMA_CONFIGS[dt].items()):

@@ -133,11 +133,11 @@ cudaError_t launch_tma(const TmaLaunch &L, cudaStream_t st)
 // Signal-group bulk-copy kernel (sfft_tma_warp.cuh): one CTA of WARPS warps
 // per SM, WPS warps per signal, each group a persistent worker.
 template <typename T, bool DIF, int WARPS, int HK, bool TM, bool RING = false, int XS = 1, int LOGN = 10,
-          int WPS = 1>
+          int WPS = 1, int PF = 0>
 cudaError_t launch_tmaw(const TmaLaunch &L, cudaStream_t st)
 {
     using Sh = TmaWShape<T, WARPS, RING, XS, LOGN, WPS>;
-    auto k = &sfft_tmaw_kernel<T, DIF, WARPS, HK, TM, RING, XS, LOGN, WPS>;
+    auto k = &sfft_tmaw_kernel<T, DIF, WARPS, HK, TM, RING, XS, LOGN, WPS, PF>;
     static Residency res;
     int dev = 0, resident = 0;
     cudaError_t e = cudaGetDevice(&dev);

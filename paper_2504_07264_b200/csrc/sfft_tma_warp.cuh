@@ -45,6 +45,12 @@ struct TmaWArgs {
     const void *tw;            // stage-major table
 };
 
+// L2 prefetch of a contiguous row (no shared memory, no completion to wait for)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
 {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -158,7 +164,11 @@ __device__ __forceinline__ int xw_phys(int e)
     return e ^ ((e >> LR) & 15);
 }
 
-template <typename T, bool DIF, int WARPS, int HK, bool TM, bool RING = false, int XS = 1, int LOGN_ = 10, int WPS = 1>
+// PF > 0 (ring mode): when a group refills its slot with signal i + NSLOT it
+// also prefetches signal i + NSLOT + PF into L2, so the later bulk copy of
+// that signal is an L2 hit.
+template <typename T, bool DIF, int WARPS, int HK, bool TM, bool RING = false, int XS = 1, int LOGN_ = 10, int WPS = 1,
+          int PF = 0>
 __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs a)
 {
     static_assert(!TM || WARPS <= 12, "TMEM factors: <= 3 warps per lane quarter");
@@ -344,6 +354,13 @@ __global__ void __launch_bounds__(32 * WARPS, 1) sfft_tmaw_kernel(const TmaWArgs
                 if constexpr (RING) {
                     rel[st] = (int)q;
                     if (i + NSLOT < nloc) issue(st, ring_row(i + NSLOT));
+                    if constexpr (PF > 0) {
+                        if (i + NSLOT + PF < nloc) {
+                            const int64_t pr_ = ring_row(i + NSLOT + PF);
+                            bulk_prefetch_l2(xr + pr_ * a.in_stride, Sh::PLANE);
+                            bulk_prefetch_l2(xi + pr_ * a.in_stride, Sh::PLANE);
+                        }
+                    }
                 } else {
                     if (k + Sh::STAGES < nk) issue(st, row + Sh::STAGES * G);
                 }

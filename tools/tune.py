@@ -17,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2504_07264_b200 as sf
 
-TMA_LR = {"f32": {5: [3], 6: [3, 2], 7: [3, 4], 8: [3, 4], 9: [3, 4], 10: [4, 3, 5], 11: [4, 3], 12: [4, 3]},
+TMA_LR = {"f32": {5: [3], 6: [3, 2], 7: [3, 4], 8: [3, 4], 9: [3, 4], 10: [4, 3, 5], 11: [4, 3], 12: [4, 3, 6]},
           "f64": {4: [2], 5: [3], 6: [3], 7: [3, 4], 8: [3, 4], 9: [3], 10: [3, 4, 5], 11: [4]}}
 
 
