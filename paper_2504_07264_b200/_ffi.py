@@ -18,7 +18,7 @@ SFFT_F32, SFFT_F64 = 0, 1
 SFFT_DIT, SFFT_DIF = 0, 1
 SFFT_FORWARD, SFFT_INVERSE = -1, 1
 SFFT_MAX_LOG2N = 30
-SFFT_KERNEL_AUTO, SFFT_KERNEL_LDG, SFFT_KERNEL_TMA, SFFT_KERNEL_PASS = 0, 1, 2, 3
+SFFT_KERNEL_AUTO, SFFT_KERNEL_LDG, SFFT_KERNEL_TMA, SFFT_KERNEL_PASS, SFFT_KERNEL_PASS2 = 0, 1, 2, 3, 4
 ABI_VERSION = 1
 
 # every symbol include/splitfft_b200.h declares: name -> (restype, argtypes)

@@ -215,6 +215,63 @@ def pass_unit(dt):
     return "\n".join(out) + "\n"
 
 
+# L2-fused group pairs (sfft_pass2.cuh): (L1, L2) of the balanced 4-group
+# splits of m = 20..28 (5,5,5,5 .. 7,7,7,7)
+PASS2_PAIRS = [(5, 5), (6, 5), (6, 6), (7, 6), (7, 7)]
+
+
+def pass2_unit(dt):
+    T = CTYPE[dt]
+    out = [
+        "// GENERATED by gen_inst.py -- do not edit",
+        "#include <atomic>",
+        '#include "sfft_pass2.cuh"',
+        '#include "sfft_launch.h"',
+        "namespace sfft {",
+        "template <int L1, int L2, bool DIF, bool SZ>",
+        f"static cudaError_t launch_pass2_{dt}(const Pass2Args &a, int64_t items, cudaStream_t st)",
+        "{",
+        f"    using Sh = P2Shape<{T}, L1, L2>;",
+        f"    auto k = sfft_pass2_kernel<{T}, L1, L2, DIF, SZ>;",
+        "    constexpr int smem = Sh::smem_bytes();",
+        "    // per-device: 'attribute set' bit + resident CTAs (published once, release/acquire)",
+        "    static std::atomic<unsigned> done_mask{0u};",
+        "    static std::atomic<int> grid_of[32];",
+        "    int dev = 0;",
+        "    cudaGetDevice(&dev);",
+        "    const unsigned bit = 1u << (dev & 31);",
+        "    if (!(done_mask.load(std::memory_order_acquire) & bit)) {",
+        "        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);",
+        "        if (e != cudaSuccess) return e;",
+        "        int per_sm = 0, sms = 0;",
+        "        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, Sh::NT, smem);",
+        "        if (e != cudaSuccess) return e;",
+        "        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);",
+        "        if (e != cudaSuccess) return e;",
+        "        if (per_sm < 1 || sms < 1) return cudaErrorInvalidConfiguration;",
+        "        grid_of[dev & 31].store(per_sm * sms, std::memory_order_relaxed);",
+        "        done_mask.fetch_or(bit, std::memory_order_release);",
+        "    }",
+        "    int64_t grid = grid_of[dev & 31].load(std::memory_order_relaxed);",
+        "    if (grid > items) grid = items;",
+        "    if (grid < 1) return cudaErrorInvalidConfiguration;",
+        "    k<<<(unsigned)grid, Sh::NT, smem, st>>>(a);",
+        "    count_launch();",
+        "    return cudaGetLastError();",
+        "}",
+        f"Pass2LaunchFn pass2_launcher_{dt}(int L1, int L2, bool dif, bool sz)",
+        "{",
+    ]
+    b = lambda v: "true" if v else "false"   # noqa: E731
+    for (l1, l2) in PASS2_PAIRS:
+        for dif in (False, True):
+            for sz in (False, True):
+                out.append(f"    if (L1 == {l1} && L2 == {l2} && dif == {b(dif)} && sz == {b(sz)}) "
+                           f"return launch_pass2_{dt}<{l1}, {l2}, {b(dif)}, {b(sz)}>;")
+    out += ["    return nullptr;", "}", "}  // namespace sfft"]
+    return "\n".join(out) + "\n"
+
+
 def tma_unit(dt):
     T = CTYPE[dt]
     out = [
@@ -313,6 +370,10 @@ def registry_unit():
         "int pass_tile(int dtype, int L) { return (dtype == 0 ? 32 : 16) >> (L >= 10 ? 1 : 0); }",
         "#endif",
         "PassLaunchFn pass_launcher(int dtype, int L) { return dtype == 0 ? pass_launcher_f32(L) : pass_launcher_f64(L); }",
+        "Pass2LaunchFn pass2_launcher(int dtype, int L1, int L2, bool dif, bool sz)",
+        "{",
+        "    return dtype == 0 ? pass2_launcher_f32(L1, L2, dif, sz) : pass2_launcher_f64(L1, L2, dif, sz);",
+        "}",
         "}  // namespace sfft",
     ]
     return "\n".join(out) + "\n"
@@ -367,6 +428,7 @@ def main(outdir):
             files[f"sfft_inst_fused_{algo}_{dt}.cu"] = fused_unit(dt, algo)
         files[f"sfft_inst_pass_{dt}.cu"] = pass_unit(dt)
         files[f"sfft_inst_tma_{dt}.cu"] = tma_unit(dt)
+        files[f"sfft_inst_pass2_{dt}.cu"] = pass2_unit(dt)
     files["sfft_inst_registry.cu"] = registry_unit()
     for name, text in files.items():
         path = os.path.join(outdir, name)

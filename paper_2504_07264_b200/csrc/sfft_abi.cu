@@ -24,6 +24,7 @@
 #include "sfft_fused.cuh"
 #include "sfft_launch.h"
 #include "sfft_pass.cuh"
+#include "sfft_pass2.cuh"
 #include "sfft_stage.cuh"
 #include "sfft_tma_host.h"
 
@@ -148,6 +149,9 @@ struct sfft_plan {
     int coarse_log = 0;
     double2 *d_fine = nullptr;
     std::vector<Group> groups;
+    // L2-fused schedule (sfft_pass2.cuh): groups = 4 balanced groups, run as
+    // two launches (groups 0+1, 2+3), one HBM sweep each
+    bool fuse2 = false;
 };
 
 namespace {
@@ -295,6 +299,45 @@ std::vector<Group> split_groups(int m)
     return g;
 }
 
+// L2-fused pairs: m = 20..28 as 4 balanced groups of 5..7 stages (the
+// pairs 0+1 and 2+3 are one sweep each).  SFFT_PASS2=0 turns it off (A/B);
+// the SFFT_PASS_SPLIT / SFFT_PASS_MAX_L developer knobs imply the unfused
+// schedule.
+constexpr int kPass2MinLog = 20, kPass2MaxLog = 28;
+// kernel=auto takes it for fp64 (6.2 vs 7.7 ms at m = 28: the fp64 pass
+// launches are issue-bound with 2 of 4 sweeps' loads exposed) and not for
+// fp32, where the per-group launches run at 0.9 of the HBM peak and the
+// persistent kernel's tile chain measured slower (profiles/r02z*);
+// SFFT_PASS2=1 / 0 forces it on / off for both.
+bool pass2_enabled(int m, int dtype)
+{
+    if (m < kPass2MinLog || m > kPass2MaxLog) return false;
+    if (getenv("SFFT_PASS_SPLIT") || getenv("SFFT_PASS_MAX_L")) return false;
+    const char *e = getenv("SFFT_PASS2");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    return dtype == SFFT_F64;
+}
+std::vector<Group> balanced4(int m)
+{
+    std::vector<Group> g;
+    int S = 0;
+    for (int k = 0; k < 4; ++k) {
+        const int L = m / 4 + (k < m % 4 ? 1 : 0);
+        g.push_back({S, L});
+        S += L;
+    }
+    return g;
+}
+int pass2_env(const char *name, int dflt, int lo, int hi)
+{
+    const char *e = getenv(name);
+    int v = e ? atoi(e) : dflt;
+    return v < lo ? lo : (v > hi ? hi : v);
+}
+constexpr int kPass2MaxSlots = 32;
+constexpr size_t kPass2CtrBytes = 2 * (1 + 2 * kPass2MaxSlots) * sizeof(unsigned);
+
 int validate_exec(const sfft_plan *p, int64_t batch, int64_t is, int64_t os, int direction)
 {
     if (!p) return fail(SFFT_EINVAL, "plan is NULL");
@@ -306,6 +349,91 @@ int validate_exec(const sfft_plan *p, int64_t batch, int64_t is, int64_t os, int
     if (direction != SFFT_FORWARD && direction != SFFT_INVERSE)
         return fail(SFFT_EINVAL, "direction must be -1 (forward) or +1 (inverse), got %d", direction);
     if (batch > (int64_t(1) << 40)) return fail(SFFT_ECAPACITY, "batch %lld exceeds the launch limit", (long long)batch);
+    return SFFT_OK;
+}
+
+// The L2-fused schedule: two persistent launches (sfft_pass2.cuh), groups
+// 0+1 then 2+3 (DIT) or 2+3 then 0+1 (DIF), through one intermediate plane
+// pair; the block scratch ring and the tile counters live in the rest of
+// the workspace.  Planar only.
+int exec_fused2(const sfft_plan *p, const void *x0, const void *x1, void *y0, void *y1, int64_t batch,
+                int64_t is, int64_t os, bool inv, double scale, void *workspace, cudaStream_t st)
+{
+    const int m = p->log2n;
+    const int64_t n = int64_t(1) << m;
+    const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
+    const int TJ = p->dtype == SFFT_F32 ? 32 : 16;
+    const size_t plane = (size_t)batch * (size_t)n * esz;
+    char *ws = (char *)workspace;
+    void *mid[2] = {ws, ws + plane};
+    char *scr = ws + 2 * plane;
+    unsigned *ctr = (unsigned *)(ws + 4 * plane);
+    const int lag = pass2_env("SFFT_P2_LAG", 4, 1, kPass2MaxSlots - 1);
+    int nslot = pass2_env("SFFT_P2_SLOTS", 8, 2, kPass2MaxSlots);
+    if (nslot <= lag) nslot = lag + 1;
+    int nslot_log = 0;
+    while ((1 << nslot_log) < nslot) ++nslot_log;   // a power of two
+    const std::vector<Group> &g = p->groups;
+    const int words = 1 + 2 * kPass2MaxSlots;
+    cudaError_t e = cudaMemsetAsync(ctr, 0, 2 * words * sizeof(unsigned), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
+    const bool dif = p->algo == SFFT_DIF;
+    for (int k = 0; k < 2; ++k) {
+        const int sg = dif ? 1 - k : k;   // super-group: groups 2sg, 2sg+1
+        const Group g1 = g[2 * sg], g2 = g[2 * sg + 1];
+        const int L = g1.L + g2.L;
+        const int64_t nb = batch * ((n >> L) / TJ);    // blocks
+        int ns_log = nslot_log;
+        while (ns_log > 0 && (int64_t(1) << (ns_log - 1)) >= nb) --ns_log;   // no more slots than blocks
+        const int ns = 1 << ns_log;
+        Pass2LaunchFn fn = pass2_launcher(p->dtype, g1.L, g2.L, dif, g1.S == 0);
+        if (!fn) return fail(SFFT_EINVAL, "no fused pass pair for L=%d+%d", g1.L, g2.L);
+        if ((size_t)ns * ((size_t)TJ << L) * esz > plane)
+            return fail(SFFT_EINVAL, "scratch ring exceeds the workspace (log2n=%d)", m);
+        Pass2Args a;
+        memset(&a, 0, sizeof a);
+        const bool first = k == 0, last = k == 1;
+        // the inverse: input planes exchanged on the first launch, output
+        // planes exchanged (and scaled) on the last
+        if (first) {
+            a.x0 = inv ? x1 : x0;
+            a.x1 = inv ? x0 : x1;
+            a.in_stride = is;
+        } else {
+            a.x0 = mid[0];
+            a.x1 = mid[1];
+            a.in_stride = n;
+        }
+        if (last) {
+            a.y0 = inv ? y1 : y0;
+            a.y1 = inv ? y0 : y1;
+            a.out_stride = os;
+        } else {
+            a.y0 = mid[0];
+            a.y1 = mid[1];
+            a.out_stride = n;
+        }
+        a.s0 = scr;
+        a.s1 = scr + plane;
+        a.ctr = ctr + k * words;
+        a.batch = batch;
+        a.m = m;
+        a.S = g1.S;
+        a.nslot_log = ns_log;
+        a.lag = lag;
+        a.scale_out = last && inv;
+        a.scale = last ? scale : 1.0;
+        a.tw = p->d_tw;
+        a.tw_cat_top = p->cat_top;
+        a.tw_top_tab = p->d_top;
+        a.coarse = p->d_coarse;
+        a.coarse_log = p->coarse_log;
+        a.fine = p->d_fine;
+        const int64_t items = nb * ((int64_t(1) << g1.L) + (int64_t(1) << g2.L));
+        if (items + 1024 * 1024 > 0xffffffffLL) return fail(SFFT_ECAPACITY, "batch %lld too large for one fused launch", (long long)batch);
+        e = fn(a, items, st);
+        if (e != cudaSuccess) return cuda_fail(e, "fused pass pair launch");
+    }
     return SFFT_OK;
 }
 
@@ -380,6 +508,7 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     if (!workspace) return fail(SFFT_EINVAL, "log2n=%d needs a workspace (sfft_workspace_bytes)", m);
     const int64_t n = int64_t(1) << m;
     const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
+    if (p->fuse2 && !il) return exec_fused2(p, x0, x1, y0, y1, batch, is, os, inv, scale, workspace, st);
     const int G = (int)p->groups.size();
     char *ws = (char *)workspace;
     const size_t plane = (size_t)batch * (size_t)n * esz;
@@ -486,8 +615,15 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
     if (dtype != SFFT_F32 && dtype != SFFT_F64) return fail(SFFT_EINVAL, "unknown dtype %d", dtype);
     const int pre_pref = (kernel >> 4) & 3;   // 0 auto, 1 off, 2 on
     kernel &= 0xf;
-    if ((kernel != SFFT_KERNEL_AUTO && kernel != SFFT_KERNEL_LDG && kernel != SFFT_KERNEL_TMA) || pre_pref == 3)
+    if ((kernel != SFFT_KERNEL_AUTO && kernel != SFFT_KERNEL_LDG && kernel != SFFT_KERNEL_TMA &&
+         kernel != SFFT_KERNEL_PASS && kernel != SFFT_KERNEL_PASS2) || pre_pref == 3)
         return fail(SFFT_EINVAL, "unknown kernel family %d", kernel);
+    if (kernel == SFFT_KERNEL_PASS && log2n <= kFusedMaxLog)
+        return fail(SFFT_EINVAL, "kernel 'pass' is the multi-launch schedule of log2n > %d, got log2n=%d",
+                    kFusedMaxLog, log2n);
+    if (kernel == SFFT_KERNEL_PASS2 && (log2n < kPass2MinLog || log2n > kPass2MaxLog))
+        return fail(SFFT_EINVAL, "kernel 'pass2' (L2-fused group pairs) needs %d <= log2n <= %d, got log2n=%d",
+                    kPass2MinLog, kPass2MaxLog, log2n);
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceCount");
@@ -551,6 +687,10 @@ int sfft_plan_create_ex(int log2n, int dtype, int algorithm, int device, int max
     } else {
         p->lr = pass_default_lr(dtype);
         p->groups = split_groups(log2n);
+        if (kernel == SFFT_KERNEL_PASS2 || (kernel != SFFT_KERNEL_PASS && pass2_enabled(log2n, dtype))) {
+            p->groups = balanced4(log2n);
+            p->fuse2 = true;
+        }
         if (dtype == SFFT_F32) {
             rc = upload_table<float>(p, kFusedMaxLog, false);
             if (rc == SFFT_OK) rc = upload_two_level(p);
@@ -586,13 +726,14 @@ int sfft_plan_info(const sfft_plan *p, int *log2n, int *dtype, int *algorithm, i
 {
     if (kernel && p)
         *kernel = p->lr_tma >= 0 ? SFFT_KERNEL_TMA
-                                   : (p->log2n <= kFusedMaxLog ? SFFT_KERNEL_LDG : SFFT_KERNEL_PASS);
+                                   : (p->log2n <= kFusedMaxLog ? SFFT_KERNEL_LDG
+                                                               : (p->fuse2 ? SFFT_KERNEL_PASS2 : SFFT_KERNEL_PASS));
     if (!p) return fail(SFFT_EINVAL, "plan is NULL");
     if (log2n) *log2n = p->log2n;
     if (dtype) *dtype = p->dtype;
     if (algorithm) *algorithm = p->algo;
     if (device) *device = p->device;
-    if (launches) *launches = p->log2n <= kFusedMaxLog ? 1 : (int)p->groups.size();
+    if (launches) *launches = p->log2n <= kFusedMaxLog ? 1 : (p->fuse2 ? 2 : (int)p->groups.size());
     if (log2_radix) *log2_radix = p->lr;
     return SFFT_OK;
 }
@@ -603,8 +744,8 @@ int sfft_exec_kernel(const sfft_plan *p, int64_t batch, int interleaved, int *fa
     if (batch < 0) return fail(SFFT_EINVAL, "batch must be >= 0, got %lld", (long long)batch);
     int fam, lr, w = 0;
     if (p->log2n > kFusedMaxLog) {
-        fam = SFFT_KERNEL_PASS;
-        lr = p->lr;
+        fam = p->fuse2 && !interleaved ? SFFT_KERNEL_PASS2 : SFFT_KERNEL_PASS;
+        lr = p->fuse2 && !interleaved ? 4 : p->lr;   // pass2: 8 threads per column, 2^(Lg-3) values each
     } else if (!interleaved && p->lr_tma >= 0 && p->kernel != SFFT_KERNEL_LDG &&
                !(p->lr_tma_small == 0 && batch < p->small_below)) {
         fam = SFFT_KERNEL_TMA;
@@ -626,8 +767,8 @@ int sfft_exec_schedule(const sfft_plan *p, int64_t batch, int interleaved, int *
     if (!p) return fail(SFFT_EINVAL, "plan is NULL");
     if (batch < 0) return fail(SFFT_EINVAL, "batch must be >= 0, got %lld", (long long)batch);
     int nl = 1, ns = 1;
-    (void)interleaved;
     if (p->log2n > kFusedMaxLog) nl = ns = (int)p->groups.size();
+    if (p->fuse2 && !interleaved) nl = ns = 2;
     if (launches) *launches = nl;
     if (sweeps) *sweeps = ns;
     return SFFT_OK;
@@ -645,6 +786,7 @@ int sfft_workspace_bytes(const sfft_plan *p, int64_t batch, size_t *bytes)
     const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
     const size_t planes = p->groups.size() >= 3 ? 4 : 2;   // ping-pong A (and B)
     *bytes = planes * (size_t)batch * ((size_t)1 << p->log2n) * esz;
+    if (p->fuse2) *bytes += kPass2CtrBytes;   // tile tickets + per-slot counters after the planes
     return SFFT_OK;
 }
 

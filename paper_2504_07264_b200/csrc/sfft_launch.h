@@ -9,12 +9,17 @@ namespace sfft {
 struct FusedArgs;
 struct PassArgs;
 struct TmaLaunch;
+struct Pass2Args;
 
 // Launch one fused kernel (N = 2^logn <= 4096) over a.batch rows.
 using FusedLaunchFn = cudaError_t (*)(const FusedArgs &a, bool dif, bool interleaved, cudaStream_t st);
 // Launch one pass group (2^L-point sub-problems) over a.batch rows.
 using PassLaunchFn = cudaError_t (*)(const PassArgs &a, bool dif, bool il_in, bool il_out,
                                      int64_t grid, cudaStream_t st);
+
+// Launch one L2-fused group pair (sfft_pass2.cuh), persistent grid capped at
+// `items` CTAs (the launcher zeroes nothing: a.ctr must be zero).
+using Pass2LaunchFn = cudaError_t (*)(const Pass2Args &a, int64_t items, cudaStream_t st);
 
 // Launch the persistent TMA-fed fused kernel (planar, 16-byte aligned rows).
 using TmaLaunchFn = cudaError_t (*)(const TmaLaunch &L, cudaStream_t st);
@@ -35,6 +40,9 @@ int pass_tile(int dtype, int L);    // TJ: sub-problems per CTA of a 2^L-point g
 int pass_default_lr(int dtype);
 PassLaunchFn pass_launcher_f32(int L);
 PassLaunchFn pass_launcher_f64(int L);
+Pass2LaunchFn pass2_launcher(int dtype, int L1, int L2, bool dif, bool sz);
+Pass2LaunchFn pass2_launcher_f32(int L1, int L2, bool dif, bool sz);
+Pass2LaunchFn pass2_launcher_f64(int L1, int L2, bool dif, bool sz);
 
 TmaLaunchFn tma_launcher(int dtype, int logn, int lr, bool dif, bool pre = false);
 TmaLaunchFn tma_launcher_f32(int logn, int lr, bool dif, bool pre);

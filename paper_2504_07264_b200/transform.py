@@ -111,9 +111,11 @@ class FftPlan:
         fam, lr, warp = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
         _ffi.check(_ffi.lib.sfft_exec_kernel(self._handle, int(batch), int(bool(interleaved)),
                                              ctypes.byref(fam), ctypes.byref(lr), ctypes.byref(warp)))
-        family = {_ffi.SFFT_KERNEL_TMA: "tma", _ffi.SFFT_KERNEL_LDG: "ldg", _ffi.SFFT_KERNEL_PASS: "pass"}[fam.value]
+        family = {_ffi.SFFT_KERNEL_TMA: "tma", _ffi.SFFT_KERNEL_LDG: "ldg", _ffi.SFFT_KERNEL_PASS: "pass",
+                  _ffi.SFFT_KERNEL_PASS2: "pass2"}[fam.value]
         name = ("sfft_tmaw_kernel" if warp.value else
-                {"tma": "sfft_tma_kernel", "ldg": "sfft_fused_kernel", "pass": "sfft_pass_kernel"}[family])
+                {"tma": "sfft_tma_kernel", "ldg": "sfft_fused_kernel", "pass": "sfft_pass_kernel",
+                 "pass2": "sfft_pass2_kernel"}[family])
         return family, lr.value, name
 
     @property
@@ -122,9 +124,10 @@ class FftPlan:
 
     @property
     def kernel(self) -> str:
-        """Kernel family used for aligned planar rows: 'tma', 'ldg' or 'pass'."""
+        """Kernel family used for aligned planar rows: 'tma', 'ldg', 'pass' or
+        'pass2' (the L2-fused group pairs)."""
         return {_ffi.SFFT_KERNEL_TMA: "tma", _ffi.SFFT_KERNEL_LDG: "ldg",
-                _ffi.SFFT_KERNEL_PASS: "pass"}[self._info()[6]]
+                _ffi.SFFT_KERNEL_PASS: "pass", _ffi.SFFT_KERNEL_PASS2: "pass2"}[self._info()[6]]
 
     def workspace_bytes(self, batch: int) -> int:
         out = ctypes.c_size_t()
@@ -169,7 +172,9 @@ def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
     the plane dtype (float64 like the reference, or float32); ``radix_log``
     overrides the register radix of the fused kernel (0 = tuned default);
     ``kernel`` picks the fused kernel family: "auto" (TMA-fed when the rows
-    allow it), "ldg" (per-thread loads) or "tma" (required);
+    allow it), "ldg" (per-thread loads) or "tma" (required); for m > 12
+    "pass" forces one launch per stage group and "pass2" the L2-fused group
+    pairs (auto's choice for 20 <= m <= 28, planar rows);
     ``prefetch_factors`` (fp32) forces fetching each pass's base factors
     before the data on/off (None = tuned default).
     """
@@ -181,7 +186,8 @@ def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
     if dtype not in _DTYPE_CODE:
         raise ValueError(f"dtype must be torch.float32 or torch.float64, got {dtype}")
     device = _resolve_device(device)
-    kernels = {"auto": _ffi.SFFT_KERNEL_AUTO, "ldg": _ffi.SFFT_KERNEL_LDG, "tma": _ffi.SFFT_KERNEL_TMA}
+    kernels = {"auto": _ffi.SFFT_KERNEL_AUTO, "ldg": _ffi.SFFT_KERNEL_LDG, "tma": _ffi.SFFT_KERNEL_TMA,
+               "pass": _ffi.SFFT_KERNEL_PASS, "pass2": _ffi.SFFT_KERNEL_PASS2}
     if kernel not in kernels:
         raise ValueError(f"kernel must be one of {sorted(kernels)}, got {kernel!r}")
     kcode = kernels[kernel] | {None: 0, False: 0x10, True: 0x20}[prefetch_factors]

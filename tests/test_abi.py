@@ -51,3 +51,16 @@ def test_plan_create_validates_before_touching_the_device():
 
 def test_launch_counter_is_exported():
     assert _ffi.launch_count() >= 0
+
+
+def test_plan_create_validates_the_large_path_kernel_choice():
+    # kernel 'pass' (one launch per group) needs log2n > 12, 'pass2' (the
+    # L2-fused group pairs) 20 <= log2n <= 28; checked before any device call
+    h = ctypes.c_void_p()
+    rc = _ffi.lib.sfft_plan_create_ex(12, 0, 0, 0, 30, 0, _ffi.SFFT_KERNEL_PASS, ctypes.byref(h))
+    assert rc == _ffi.SFFT_EINVAL and b"log2n > 12" in _ffi.lib.sfft_last_error()
+    for m in (19, 29):
+        rc = _ffi.lib.sfft_plan_create_ex(m, 0, 0, 0, 30, 0, _ffi.SFFT_KERNEL_PASS2, ctypes.byref(h))
+        assert rc == _ffi.SFFT_EINVAL and b"20 <= log2n <= 28" in _ffi.lib.sfft_last_error()
+    rc = _ffi.lib.sfft_plan_create_ex(20, 0, 0, 0, 30, 0, 5, ctypes.byref(h))
+    assert rc == _ffi.SFFT_EINVAL and b"unknown kernel family" in _ffi.lib.sfft_last_error()
