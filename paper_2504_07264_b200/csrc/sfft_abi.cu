@@ -371,6 +371,7 @@ int exec_fused2(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     const int lag = pass2_env("SFFT_P2_LAG", 4, 1, kPass2MaxSlots - 1);
     int nslot = pass2_env("SFFT_P2_SLOTS", 8, 2, kPass2MaxSlots);
     if (nslot <= lag) nslot = lag + 1;
+    const int flags = pass2_env("SFFT_P2_FLAGS", 0, 0, 7);
     int nslot_log = 0;
     while ((1 << nslot_log) < nslot) ++nslot_log;   // a power of two
     const std::vector<Group> &g = p->groups;
@@ -413,8 +414,8 @@ int exec_fused2(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
             a.y1 = mid[1];
             a.out_stride = n;
         }
-        a.s0 = scr;
-        a.s1 = scr + plane;
+        a.s0 = scr;   // (re, im) pairs: the ring takes up to two planes' worth
+        a.s1 = nullptr;
         a.ctr = ctr + k * words;
         a.batch = batch;
         a.m = m;
@@ -423,6 +424,10 @@ int exec_fused2(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         a.lag = lag;
         a.scale_out = last && inv;
         a.scale = last ? scale : 1.0;
+        a.flags = flags;
+        // the L2 prefetch issues 128-byte bulk requests: 16-byte aligned source runs only
+        if ((((uintptr_t)a.x0 | (uintptr_t)a.x1) & 15) || (batch > 1 && ((size_t)a.in_stride * esz) % 16))
+            a.flags &= ~P2_PREFETCH;
         a.tw = p->d_tw;
         a.tw_cat_top = p->cat_top;
         a.tw_top_tab = p->d_top;

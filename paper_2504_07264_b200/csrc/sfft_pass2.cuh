@@ -16,12 +16,14 @@
 // block) stays in L2, so each pair of groups costs one HBM read and one
 // HBM write of the row instead of two of each.
 //
-// Scratch layout of a block (columns jl < TJ = the block's sub-problems,
-// E2 < 2^L2, o < 2^L1):
-//   S > 0:  ((E2 << L1) + o) * TJ + jl   -- both sides 128-byte runs over jl
+// Scratch layout of a block, (re, im) pairs (one 64/128-bit access per complex
+// value; every scratch stride is a compile-time constant, so the scratch
+// side of a tile is addressed as one per-thread base plus immediates)
+// (columns jl < TJ = the block's sub-problems, E2 < 2^L2, o < 2^L1):
+//   S > 0:  ((E2 << L1) + o) * TJ + jl   -- both sides 256-byte runs over jl
 //   S = 0:  ((jl << L2) + E2 << L1) + o  -- the first group's outputs are rows
 //           of 2^L1 per sub-problem (the S = 0 transpose); the second group
-//           reads 128-byte runs over o
+//           reads 256-byte runs over o
 // The tiles are the pass kernel's tiles (TJ columns x 2^Lg points, register
 // passes + shared exchanges, the same factor formation), so every output
 // is bit-identical to the multi-launch schedule with the same groups.
@@ -45,12 +47,13 @@ namespace sfft {
 struct Pass2Args {
     const void *x0, *x1;   // super-group source planes (the host exchanges them for the inverse)
     void *y0, *y1;         // destination planes
-    void *s0, *s1;         // scratch ring planes: nslot blocks of TJ * 2^L elements
+    void *s0, *s1;         // s0: scratch ring of nslot blocks of TJ * 2^L (re, im) pairs (s1 unused)
     unsigned *ctr;         // [0] ticket, [1 + slot] first-group tiles done, [1 + nslot + slot] second
     int64_t batch, in_stride, out_stride;
     int m, S;              // log2 N, stage offset of the super-group
     int nslot_log, lag;    // ring of 2^nslot_log block slots, second phase `lag` blocks behind
     int scale_out;         // multiply the destination by `scale` (the inverse's last launch)
+    int flags;             // P2_DEFER | P2_PREFETCH (see the kernel)
     double scale;
     const void *tw;        // as PassArgs
     int tw_cat_top;
@@ -59,6 +62,14 @@ struct Pass2Args {
     int coarse_log;
     const double2 *fine;
 };
+
+// flags: publish a tile's completion after the NEXT tile's loads are issued
+// (the release fence then waits next to loads every warp waits for, instead
+// of holding warp 0 back at the tile boundary); prefetch the next tile's
+// HBM-side source runs into L2 once its ticket is known (one 128-byte line
+// per thread with prefetch.global.L2; P2_PREFETCH_BULK: cp.async.bulk.prefetch,
+// which the uniform datapath serialises lane by lane -- measured, not used).
+constexpr int P2_DEFER = 1, P2_PREFETCH = 2, P2_PREFETCH_BULK = 4;
 
 template <typename T> struct P2TJ { static constexpr int value = sizeof(T) == 4 ? 32 : 16; };
 
@@ -96,30 +107,22 @@ __device__ __forceinline__ typename PassTw<T, S0G>::type make_p2_tw(const Pass2A
     return tw;
 }
 
-template <bool SCR, typename T>
-__device__ __forceinline__ T p2_ld(const T *p)
-{
-    if constexpr (SCR) return __ldcg(p);   // written by other SMs during this kernel: L2, never L1
-    else return ld_stream(p);
-}
-
-template <bool SCR, typename T>
-__device__ __forceinline__ void p2_st(T *p, T v)
-{
-    if constexpr (SCR) __stcg(p, v);      // the block scratch: default L2 policy, read back soon
-    else st_stream(p, v);
-}
-
 // One tile: TJ columns of 2^L-point sub-problems of group (S, L), column jl's
 // factor column c0 + jl (S > 0).  Column side: element e of column jl at
 // base + jl + e * stride; row side (the S = 0 group: DIT destination, DIF
 // source): element o of column jl at base + jl * stride + o.
-// `mid()` runs once, after the first register pass (the scheduler's
-// look-ahead for the next tile, off the tile's critical path).
-template <typename T, int L, bool DIF, bool S0G, bool IN_SCR, bool OUT_SCR, typename Mid>
+// Scheduler hooks, each run once per tile: `ldh()` after the tile's global
+// loads (and column-factor lookups) are issued, `mid()` after the first
+// register pass (the look-ahead for the next tile, off the tile's critical
+// path), `px()` after the CTA barrier that follows `mid()`.
+// The scratch side (IN_SCR: source, OUT_SCR: destination) is `scr`, pairs
+// with the compile-time element stride SSTR; the plane pointers and the
+// runtime stride of that side are unused.
+template <typename T, int L, bool DIF, bool S0G, bool IN_SCR, bool OUT_SCR, uint32_t SSTR, typename Ldh,
+          typename Mid, typename Px>
 __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr, T *orr, T *oi, uint32_t ostr,
-                                        int S, uint32_t c0, const Pass2Args &a, unsigned char *smem_raw,
-                                        const Mid &mid)
+                                        vec2_t<T> *scr, int S, uint32_t c0, const Pass2Args &a,
+                                        unsigned char *smem_raw, const Ldh &ldh, const Mid &mid, const Px &px)
 {
     constexpr int TJ = P2TJ<T>::value, P = 8, SUB = 1 << L, LR = L - 3, R = 1 << LR, NT = TJ * P;
     constexpr int RS = TJ + 1, NPI = (L + LR - 1) / LR;
@@ -138,13 +141,33 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
     constexpr bool CST = FactorTw<T>::value && !S0G;
     const uint32_t is_b = istr * (uint32_t)sizeof(T), os_b = ostr * (uint32_t)sizeof(T);
 
-    auto put = [&](T *pr, T *pi, V w) {
-        if (scale_out) {
-            w.x *= scale;
-            w.y *= scale;
+    // source element at `k` strides / `off` elements from the thread's base
+    // (planes pr, pi or scratch pairs ps); destination likewise
+    auto get_k = [&](const T *pr, const T *pi, const V *ps, uint32_t k) {
+        V w;
+        if constexpr (IN_SCR) {
+            w = __ldcg(ps + k * SSTR);   // written by other SMs during this kernel: L2, never L1
+        } else {
+            w.x = ld_stream(at_stride(pr, is_b, k));
+            w.y = ld_stream(at_stride(pi, is_b, k));
         }
-        p2_st<OUT_SCR>(pr, w.x);
-        p2_st<OUT_SCR>(pi, w.y);
+        return w;
+    };
+    auto put = [&](T *pr, T *pi, V *ps, V w) {
+        if constexpr (OUT_SCR) {
+            __stcg(ps, w);   // the block scratch: default L2 policy, read back soon
+        } else {
+            if (scale_out) {
+                w.x *= scale;
+                w.y *= scale;
+            }
+            st_stream(pr, w.x);
+            st_stream(pi, w.y);
+        }
+    };
+    auto put_k = [&](T *pr, T *pi, V *ps, uint32_t k, V w) {
+        if constexpr (OUT_SCR) put(nullptr, nullptr, ps + k * SSTR, w);
+        else put(at_stride(pr, os_b, k), at_stride(pi, os_b, k), nullptr, w);
     };
     auto stage_columns = [&]() {
         if constexpr (CST) {
@@ -152,7 +175,10 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
                 const int st = k / TJ, l = k - st * TJ;
                 cs[k] = tw.get(S + 1 + st, (I)(c0 + (uint32_t)l));
             }
+            ldh();
             __syncthreads();
+        } else {
+            ldh();
         }
     };
     auto column_factors = [&](int sp, int KP, int jp, V *cf) {
@@ -173,8 +199,9 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
     V v[R];
     if constexpr (!DIF) {
         // column-side source: element (t + k) of column jl
-        const T *in_r = ir + jl + (size_t)t * istr;
-        const T *in_i = ii + jl + (size_t)t * istr;
+        const T *in_r = IN_SCR ? nullptr : ir + jl + (size_t)t * istr;
+        const T *in_i = IN_SCR ? nullptr : ii + jl + (size_t)t * istr;
+        const V *in_s = IN_SCR ? scr + jl + t * SSTR : nullptr;
         static_for<0, NPI>([&](auto PPC) {
             constexpr int pp = decltype(PPC)::value;
             constexpr int sp = pp * LR, KP = cmin(LR, L - sp), RP = 1 << KP, U = R / RP, nsp = 1 << sp;
@@ -186,8 +213,7 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
                 for (int r = 0; r < RP; ++r) {
                     if constexpr (pp == 0) {
                         const uint32_t k = (uint32_t)(P * u + r * (SUB / RP));
-                        v[u * RP + r].x = p2_ld<IN_SCR>(at_stride(in_r, is_b, k));
-                        v[u * RP + r].y = p2_ld<IN_SCR>(at_stride(in_i, is_b, k));
+                        v[u * RP + r] = get_k(in_r, in_i, in_s, k);
                     } else {
                         v[u * RP + r] = sx[(jp + r * (SUB / RP)) * RS + jl];
                     }
@@ -213,15 +239,17 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
                     for (int f = 0; f < RP; ++f) sx[(base + nsp * f) * RS + jl] = v[u * RP + brev(f, KP)];
                 }
                 __syncthreads();
+                if constexpr (pp == 0) px();
             } else {
-                T *out_r = orr + jl + (size_t)t * ostr;
-                T *out_i = oi + jl + (size_t)t * ostr;
+                T *out_r = OUT_SCR ? nullptr : orr + jl + (size_t)t * ostr;
+                T *out_i = OUT_SCR ? nullptr : oi + jl + (size_t)t * ostr;
+                V *out_s = OUT_SCR ? scr + jl + t * SSTR : nullptr;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
 #pragma unroll
                     for (int f = 0; f < RP; ++f) {
                         const uint32_t k = (uint32_t)(P * u + nsp * f);
-                        put(at_stride(out_r, os_b, k), at_stride(out_i, os_b, k), v[u * RP + brev(f, KP)]);
+                        put_k(out_r, out_i, out_s, k, v[u * RP + brev(f, KP)]);
                     }
                 }
             }
@@ -231,8 +259,12 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
 #pragma unroll
             for (int kk = 0; kk < R; ++kk) {
                 const int k = tid + kk * NT, jj = k >> L, o = k & (SUB - 1);
-                const size_t off = (size_t)jj * ostr + o;
-                put(orr + off, oi + off, sx[o * RS + jj]);
+                if constexpr (OUT_SCR) {
+                    put(nullptr, nullptr, scr + (uint32_t)jj * SSTR + o, sx[o * RS + jj]);
+                } else {
+                    const size_t off = (size_t)jj * ostr + o;
+                    put(orr + off, oi + off, nullptr, sx[o * RS + jj]);
+                }
             }
         }
     } else {
@@ -241,10 +273,15 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
 #pragma unroll
             for (int kk = 0; kk < R; ++kk) {
                 const int k = tid + kk * NT, jj = k >> L, o = k & (SUB - 1);
-                const size_t off = (size_t)jj * istr + o;
-                v[kk].x = p2_ld<IN_SCR>(ir + off);
-                v[kk].y = p2_ld<IN_SCR>(ii + off);
+                if constexpr (IN_SCR) {
+                    v[kk] = __ldcg(scr + (uint32_t)jj * SSTR + o);
+                } else {
+                    const size_t off = (size_t)jj * istr + o;
+                    v[kk].x = ld_stream(ir + off);
+                    v[kk].y = ld_stream(ii + off);
+                }
             }
+            ldh();
 #pragma unroll
             for (int kk = 0; kk < R; ++kk) {
                 const int k = tid + kk * NT, jj = k >> L, o = k & (SUB - 1);
@@ -252,7 +289,8 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
             }
             __syncthreads();
         }
-        const T *in_r = ir + jl, *in_i = ii + jl;
+        const T *in_r = IN_SCR ? nullptr : ir + jl, *in_i = IN_SCR ? nullptr : ii + jl;
+        const V *in_s = IN_SCR ? scr + jl : nullptr;
         static_for<0, NPI>([&](auto QC) {
             constexpr int pp = NPI - 1 - decltype(QC)::value;
             constexpr int sp = pp * LR, KP = cmin(LR, L - sp), RP = 1 << KP, U = R / RP, nsp = 1 << sp;
@@ -265,16 +303,19 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
                 for (int f = 0; f < RP; ++f) {
                     const int d = u * RP + brev(f, KP);
                     if constexpr (first && !S0G) {
-                        const T *pr = in_r + (size_t)base * istr, *pi = in_i + (size_t)base * istr;
                         const uint32_t k = (uint32_t)(nsp * f);
-                        v[d].x = p2_ld<IN_SCR>(at_stride(pr, is_b, k));
-                        v[d].y = p2_ld<IN_SCR>(at_stride(pi, is_b, k));
+                        if constexpr (IN_SCR) {
+                            v[d] = get_k(nullptr, nullptr, in_s + (uint32_t)base * SSTR, k);
+                        } else {
+                            const T *pr = in_r + (size_t)base * istr, *pi = in_i + (size_t)base * istr;
+                            v[d] = get_k(pr, pi, nullptr, k);
+                        }
                     } else {
                         v[d] = sx[(base + nsp * f) * RS + jl];
                     }
                 }
             }
-            if constexpr (first) stage_columns();
+            if constexpr (first && !S0G) stage_columns();
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int jp = t + P * u;
@@ -293,15 +334,17 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
                     for (int r = 0; r < RP; ++r) sx[(jp + r * (SUB / RP)) * RS + jl] = v[u * RP + r];
                 }
                 __syncthreads();
+                if constexpr (first) px();
             } else {
-                T *out_r = orr + jl + (size_t)t * ostr;
-                T *out_i = oi + jl + (size_t)t * ostr;
+                T *out_r = OUT_SCR ? nullptr : orr + jl + (size_t)t * ostr;
+                T *out_i = OUT_SCR ? nullptr : oi + jl + (size_t)t * ostr;
+                V *out_s = OUT_SCR ? scr + jl + t * SSTR : nullptr;
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
 #pragma unroll
                     for (int r = 0; r < RP; ++r) {
                         const uint32_t k = (uint32_t)(P * u + r * (SUB / RP));
-                        put(at_stride(out_r, os_b, k), at_stride(out_i, os_b, k), v[u * RP + r]);
+                        put_k(out_r, out_i, out_s, k, v[u * RP + r]);
                     }
                 }
             }
@@ -323,6 +366,12 @@ __device__ __forceinline__ unsigned p2_ld_relaxed(const unsigned *p)
 __device__ __forceinline__ void p2_signal(unsigned *p)
 {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+
+// L2 prefetch of one contiguous run (no destination, nothing to wait for)
+__device__ __forceinline__ void p2_prefetch_run(const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // One scheduled tile: phase (0: the group run first), block, tile index, and
@@ -412,6 +461,50 @@ sfft_pass2_kernel(const Pass2Args a)
     };
 
     __shared__ int s_ok[2];
+    __shared__ const char *s_pf[2];    // the next tile's HBM-side source runs (P2_PREFETCH)
+    __shared__ uint32_t s_pf_stride;
+    __shared__ int s_pf_rows;
+
+    // the two groups' tile geometry (see the comment above the kernel)
+    struct Geom {
+        size_t so, xo;
+        uint32_t xs, cc;
+    };
+    auto geom = [&](bool first_group, uint32_t tile, uint32_t J0) {
+        Geom g;
+        if (first_group) {
+            const uint32_t E2 = tile;
+            g.xo = J0 + (size_t)E2 * NJ;
+            g.xs = NJ << L2;
+            g.so = SZ ? ((size_t)E2 << L1) : (((size_t)E2 << L1) * TJ);
+            g.cc = J0 & ((1u << S) - 1u);
+        } else {
+            const uint32_t u = tile;
+            if constexpr (SZ) {
+                constexpr int CPT = (1 << L1) / TJ;   // tiles per column
+                const uint32_t jl = u / CPT, o0 = (u % CPT) * TJ;
+                g.so = ((size_t)jl << L) + o0;
+                g.xo = ((size_t)(J0 + jl) << L) + o0;
+                g.xs = 1u << L1;
+                g.cc = o0;
+            } else {
+                g.so = (size_t)u * TJ;
+                const uint32_t jm = J0 & ((1u << S) - 1u);
+                g.xo = (((size_t)(J0 >> S)) << (S + L)) + jm + ((size_t)u << S);
+                g.xs = 1u << (S + L1);
+                g.cc = jm + (u << S);
+            }
+        }
+        return g;
+    };
+
+    int pend = 0;   // thread 0: index in ctr[] of a finished tile's counter, not yet published (P2_DEFER)
+    auto flush = [&]() {
+        if (pend) {
+            p2_signal(a.ctr + pend);
+            pend = 0;
+        }
+    };
     if (tid == 0) {
         s_item[0] = atomicAdd(a.ctr, 1u);
         s_ok[0] = 0;
@@ -419,78 +512,94 @@ sfft_pass2_kernel(const Pass2Args a)
     __syncthreads();
     for (int it = 0;; ++it) {
         const uint32_t g = s_item[it & 1];
-        if (g >= total) return;
+        if (g >= total) {
+            if (tid == 0) flush();
+            return;
+        }
         const bool ok = s_ok[it & 1] != 0;
         const P2Item q = decode(g);
         // the next ticket: issued now, consumed after the first register pass
         unsigned nxt = 0;
         if (tid == 0) nxt = atomicAdd(a.ctr, 1u);
         if (!ok) {   // the look-ahead poll did not see the dependency satisfied
-            if (tid == 0 && q.dep)
-                while (p2_ld_relaxed(q.dep) < q.target) __nanosleep(64);
+            if (tid == 0) {
+                flush();   // what this CTA still owes may be what it is about to wait for
+                if (q.dep)
+                    while (p2_ld_relaxed(q.dep) < q.target) __nanosleep(64);
+            }
             __syncthreads();
         }
+        auto ldh = [&]() {
+            if (tid == 0) flush();
+        };
         // look-ahead: decode the next ticket and poll its dependency once;
         // the poll's value is only needed at the end of this tile
         unsigned polled = 0, want = 0;
         bool nodep = true;
         auto mid = [&]() {
-            if (tid == 0 && nxt < total) {
-                const P2Item n = decode(nxt);
-                nodep = n.dep == nullptr;
-                if (!nodep) {
-                    polled = p2_ld_relaxed(n.dep);
-                    want = n.target;
+            if (tid == 0) {
+                int pf_rows = 0;
+                if (nxt < total) {
+                    const P2Item n = decode(nxt);
+                    nodep = n.dep == nullptr;
+                    if (!nodep) {
+                        polled = p2_ld_relaxed(n.dep);
+                        want = n.target;
+                    }
+                    if ((a.flags & P2_PREFETCH) && n.ph == 0) {   // phase 0 reads the super-group's source planes
+                        const int64_t nrow = n.b >> (m - L - LTJ);
+                        const uint32_t nJ0 = ((uint32_t)n.b & (nbr - 1u)) * TJ;
+                        const Geom ng = geom(!DIF, (uint32_t)n.tile, nJ0);
+                        s_pf[0] = (const char *)((const T *)a.x0 + nrow * a.in_stride + ng.xo);
+                        s_pf[1] = (const char *)((const T *)a.x1 + nrow * a.in_stride + ng.xo);
+                        s_pf_stride = ng.xs * (uint32_t)sizeof(T);
+                        pf_rows = 1 << (DIF ? L2 : L1);
+                    }
+                }
+                if (a.flags & P2_PREFETCH) s_pf_rows = pf_rows;
+            }
+        };
+        auto px = [&]() {
+            if (a.flags & P2_PREFETCH) {
+                const int rows = s_pf_rows;
+                for (int k = tid; k < 2 * rows; k += Sh::NT) {
+                    const int pl = k >= rows, e = k - pl * rows;
+                    const char *run = s_pf[pl] + (size_t)e * s_pf_stride;   // one 128-byte line
+                    if (a.flags & P2_PREFETCH_BULK)
+                        p2_prefetch_run(run, TJ * (uint32_t)sizeof(T));
+                    else
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(run) : "memory");
                 }
             }
         };
 
         const int64_t row = q.b >> (m - L - LTJ);
         const uint32_t J0 = ((uint32_t)q.b & (nbr - 1u)) * TJ;
-        T *sr = (T *)a.s0 + q.slot * slot_elems, *si = (T *)a.s1 + q.slot * slot_elems;
+        vec2_t<T> *sc = (vec2_t<T> *)a.s0 + q.slot * slot_elems;
         const bool first_group = (q.ph == 0) != DIF;   // group (S, L1)?
+        const Geom gm = geom(first_group, (uint32_t)q.tile, J0);
+        // compile-time scratch strides of the two groups (see geom: g.ss)
+        constexpr uint32_t SS1 = SZ ? (1u << L) : (uint32_t)TJ;
+        constexpr uint32_t SS2 = SZ ? (1u << L1) : ((uint32_t)TJ << L1);
         if (first_group) {
-            const uint32_t E2 = (uint32_t)q.tile;
-            const size_t xo = J0 + (size_t)E2 * NJ;
-            const uint32_t xs = NJ << L2;
-            const size_t so = SZ ? ((size_t)E2 << L1) : (((size_t)E2 << L1) * TJ);
-            const uint32_t ss = SZ ? (1u << L) : (uint32_t)TJ;
-            const uint32_t cc = J0 & ((1u << S) - 1u);
             if constexpr (!DIF) {
-                const T *xr = (const T *)a.x0 + row * a.in_stride + xo, *xi = (const T *)a.x1 + row * a.in_stride + xo;
-                p2_tile<T, L1, false, SZ, false, true>(xr, xi, xs, sr + so, si + so, ss, S, cc, a, smem_raw, mid);
+                const T *xr = (const T *)a.x0 + row * a.in_stride + gm.xo, *xi = (const T *)a.x1 + row * a.in_stride + gm.xo;
+                p2_tile<T, L1, false, SZ, false, true, SS1>(xr, xi, gm.xs, nullptr, nullptr, 0u, sc + gm.so, S, gm.cc,
+                                                            a, smem_raw, ldh, mid, px);
             } else {
-                T *yr = (T *)a.y0 + row * a.out_stride + xo, *yi = (T *)a.y1 + row * a.out_stride + xo;
-                p2_tile<T, L1, true, SZ, true, false>(sr + so, si + so, ss, yr, yi, xs, S, cc, a, smem_raw, mid);
+                T *yr = (T *)a.y0 + row * a.out_stride + gm.xo, *yi = (T *)a.y1 + row * a.out_stride + gm.xo;
+                p2_tile<T, L1, true, SZ, true, false, SS1>(nullptr, nullptr, 0u, yr, yi, gm.xs, sc + gm.so, S, gm.cc,
+                                                           a, smem_raw, ldh, mid, px);
             }
         } else {
-            const uint32_t u = (uint32_t)q.tile;
-            size_t so, xo;
-            uint32_t ss, xs, cc;
-            if constexpr (SZ) {
-                constexpr int CPT = (1 << L1) / TJ;   // tiles per column
-                const uint32_t jl = u / CPT, o0 = (u % CPT) * TJ;
-                so = ((size_t)jl << L) + o0;
-                ss = 1u << L1;
-                xo = ((size_t)(J0 + jl) << L) + o0;
-                xs = 1u << L1;
-                cc = o0;
-            } else {
-                so = (size_t)u * TJ;
-                ss = (uint32_t)TJ << L1;
-                const uint32_t jm = J0 & ((1u << S) - 1u);
-                xo = (((size_t)(J0 >> S)) << (S + L)) + jm + ((size_t)u << S);
-                xs = 1u << (S + L1);
-                cc = jm + (u << S);
-            }
             if constexpr (!DIF) {
-                T *yr = (T *)a.y0 + row * a.out_stride + xo, *yi = (T *)a.y1 + row * a.out_stride + xo;
-                p2_tile<T, L2, false, false, true, false>(sr + so, si + so, ss, yr, yi, xs, S + L1, cc, a, smem_raw,
-                                                          mid);
+                T *yr = (T *)a.y0 + row * a.out_stride + gm.xo, *yi = (T *)a.y1 + row * a.out_stride + gm.xo;
+                p2_tile<T, L2, false, false, true, false, SS2>(nullptr, nullptr, 0u, yr, yi, gm.xs, sc + gm.so, S + L1,
+                                                               gm.cc, a, smem_raw, ldh, mid, px);
             } else {
-                const T *xr = (const T *)a.x0 + row * a.in_stride + xo, *xi = (const T *)a.x1 + row * a.in_stride + xo;
-                p2_tile<T, L2, true, false, false, true>(xr, xi, xs, sr + so, si + so, ss, S + L1, cc, a, smem_raw,
-                                                         mid);
+                const T *xr = (const T *)a.x0 + row * a.in_stride + gm.xo, *xi = (const T *)a.x1 + row * a.in_stride + gm.xo;
+                p2_tile<T, L2, true, false, false, true, SS2>(xr, xi, gm.xs, nullptr, nullptr, 0u, sc + gm.so, S + L1,
+                                                              gm.cc, a, smem_raw, ldh, mid, px);
             }
         }
         if (tid == 0) {
@@ -498,7 +607,13 @@ sfft_pass2_kernel(const Pass2Args a)
             s_ok[(it + 1) & 1] = nodep || polled >= want;
         }
         __syncthreads();   // every thread's stores of this tile issued; shared reads done
-        if (tid == 0) p2_signal(q.ph == 0 ? doneA + q.slot : doneB + q.slot);
+        if (tid == 0) {
+            const int c = 1 + (q.ph == 0 ? 0 : nslot) + q.slot;   // doneA / doneB
+            if (a.flags & P2_DEFER)
+                pend = c;   // published by flush(): after the next tile's loads, or before a wait / the exit
+            else
+                p2_signal(a.ctr + c);
+        }
     }
 }
 

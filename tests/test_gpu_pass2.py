@@ -132,7 +132,16 @@ def test_fused_strided_rows_and_in_place(cuda, dtype):
 KNOBS = {"lag1_slots2": {"SFFT_P2_LAG": "1", "SFFT_P2_SLOTS": "2"},
          "lag7_slots8": {"SFFT_P2_LAG": "7", "SFFT_P2_SLOTS": "8"},
          "lag3_slots5": {"SFFT_P2_LAG": "3", "SFFT_P2_SLOTS": "5"},
-         "lag3_slots32": {"SFFT_P2_LAG": "3", "SFFT_P2_SLOTS": "32"}}
+         "lag3_slots32": {"SFFT_P2_LAG": "3", "SFFT_P2_SLOTS": "32"},
+         # scheduler variants: completion published at the tile boundary (0) /
+         # deferred behind the next tile's loads (1), without / with the L2
+         # prefetch of the next tile's source runs (2); a tight ring makes the
+         # deferred publication go through its flush-before-wait path
+         "flags0": {"SFFT_P2_FLAGS": "0"},
+         "flags1_lag1_slots2": {"SFFT_P2_FLAGS": "1", "SFFT_P2_LAG": "1", "SFFT_P2_SLOTS": "2"},
+         "flags2": {"SFFT_P2_FLAGS": "2"},
+         "flags3": {"SFFT_P2_FLAGS": "3"},
+         "flags3_lag8_slots16": {"SFFT_P2_FLAGS": "3", "SFFT_P2_LAG": "8", "SFFT_P2_SLOTS": "16"}}
 
 
 @pytest.mark.parametrize("knob", sorted(KNOBS))
