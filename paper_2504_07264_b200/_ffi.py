@@ -12,6 +12,8 @@ import os
 from .errors import CapacityError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsplitfft_b200.so")
+# developer knob (A/B of two builds on one box, tools/p2_sweep.py): another build of the same library
+LIB_PATH = os.environ.get("SFFT_B200_LIB", LIB_PATH)
 
 SFFT_OK, SFFT_EINVAL, SFFT_ECAPACITY, SFFT_ECUDA = 0, 1, 2, 3
 SFFT_F32, SFFT_F64 = 0, 1

@@ -371,7 +371,7 @@ int exec_fused2(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     const int lag = pass2_env("SFFT_P2_LAG", 4, 1, kPass2MaxSlots - 1);
     int nslot = pass2_env("SFFT_P2_SLOTS", 8, 2, kPass2MaxSlots);
     if (nslot <= lag) nslot = lag + 1;
-    const int flags = pass2_env("SFFT_P2_FLAGS", 0, 0, 7);
+    const int flags = pass2_env("SFFT_P2_FLAGS", 0, 0, 1);
     int nslot_log = 0;
     while ((1 << nslot_log) < nslot) ++nslot_log;   // a power of two
     const std::vector<Group> &g = p->groups;
@@ -425,9 +425,6 @@ int exec_fused2(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         a.scale_out = last && inv;
         a.scale = last ? scale : 1.0;
         a.flags = flags;
-        // the L2 prefetch issues 128-byte bulk requests: 16-byte aligned source runs only
-        if ((((uintptr_t)a.x0 | (uintptr_t)a.x1) & 15) || (batch > 1 && ((size_t)a.in_stride * esz) % 16))
-            a.flags &= ~P2_PREFETCH;
         a.tw = p->d_tw;
         a.tw_cat_top = p->cat_top;
         a.tw_top_tab = p->d_top;
@@ -513,7 +510,11 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     if (!workspace) return fail(SFFT_EINVAL, "log2n=%d needs a workspace (sfft_workspace_bytes)", m);
     const int64_t n = int64_t(1) << m;
     const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
-    if (p->fuse2 && !il) return exec_fused2(p, x0, x1, y0, y1, batch, is, os, inv, scale, workspace, st);
+    // the fused pairs copy their source tiles with 16-byte cp.async: rows that
+    // are not 16-byte aligned take the one-launch-per-group schedule (same groups)
+    const bool rows16 = !(((uintptr_t)x0 | (uintptr_t)x1) & 15) && (batch == 1 || ((size_t)is * esz) % 16 == 0);
+    if (p->fuse2 && !il && rows16)
+        return exec_fused2(p, x0, x1, y0, y1, batch, is, os, inv, scale, workspace, st);
     const int G = (int)p->groups.size();
     char *ws = (char *)workspace;
     const size_t plane = (size_t)batch * (size_t)n * esz;
