@@ -304,11 +304,14 @@ std::vector<Group> split_groups(int m)
 // the SFFT_PASS_SPLIT / SFFT_PASS_MAX_L developer knobs imply the unfused
 // schedule.
 constexpr int kPass2MinLog = 20, kPass2MaxLog = 28;
-// kernel=auto takes it for fp64 (6.2 vs 7.7 ms at m = 28: the fp64 pass
-// launches are issue-bound with 2 of 4 sweeps' loads exposed) and not for
-// fp32, where the per-group launches run at 0.9 of the HBM peak and the
-// persistent kernel's tile chain measured slower (profiles/r02z*);
-// SFFT_PASS2=1 / 0 forces it on / off for both.
+// kernel=auto takes it only for fp64 at m = 28 (6.2-6.9 vs 7.7 ms: the fp64
+// pass launches are issue-bound with 2 of 4 sweeps' loads exposed).  Below
+// that the per-group launches win by 1.5-4x (m = 26: 2.0 vs 3.0 ms, m = 20:
+// 0.045 vs 0.17 ms -- smaller rows leave the persistent kernel few blocks
+// and half-size tiles), and fp32 per-group launches run at 0.9 of the HBM
+// peak while the persistent tile chain is latency-bound (m = 28: 2.71 vs
+// 2.79 ms; profiles/r02z*, r02aa-ac).  SFFT_PASS2=1 / 0 forces it on / off
+// for every size and type it supports.
 bool pass2_enabled(int m, int dtype)
 {
     if (m < kPass2MinLog || m > kPass2MaxLog) return false;
@@ -316,7 +319,7 @@ bool pass2_enabled(int m, int dtype)
     const char *e = getenv("SFFT_PASS2");
     if (e && e[0] == '0') return false;
     if (e && e[0] == '1') return true;
-    return dtype == SFFT_F64;
+    return dtype == SFFT_F64 && m == 28;
 }
 std::vector<Group> balanced4(int m)
 {
@@ -368,10 +371,14 @@ int exec_fused2(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     void *mid[2] = {ws, ws + plane};
     char *scr = ws + 2 * plane;
     unsigned *ctr = (unsigned *)(ws + 4 * plane);
-    const int lag = pass2_env("SFFT_P2_LAG", 4, 1, kPass2MaxSlots - 1);
-    int nslot = pass2_env("SFFT_P2_SLOTS", 8, 2, kPass2MaxSlots);
+    // ring geometry and scheduler variant (profiles/r02ab_*): fp32 6 blocks
+    // behind in a 16-slot ring with the L2 prefetch of the next tile; fp64 4
+    // behind in 8 slots, no prefetch
+    const bool f32 = p->dtype == SFFT_F32;
+    const int lag = pass2_env("SFFT_P2_LAG", f32 ? 6 : 4, 1, kPass2MaxSlots - 1);
+    int nslot = pass2_env("SFFT_P2_SLOTS", f32 ? 16 : 8, 2, kPass2MaxSlots);
     if (nslot <= lag) nslot = lag + 1;
-    const int flags = pass2_env("SFFT_P2_FLAGS", 0, 0, 1);
+    const int flags = pass2_env("SFFT_P2_FLAGS", f32 ? P2_PREFETCH : 0, 0, 7);
     int nslot_log = 0;
     while ((1 << nslot_log) < nslot) ++nslot_log;   // a power of two
     const std::vector<Group> &g = p->groups;
@@ -425,6 +432,9 @@ int exec_fused2(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
         a.scale_out = last && inv;
         a.scale = last ? scale : 1.0;
         a.flags = flags;
+        // the L2 prefetch issues 128-byte bulk requests: 16-byte aligned source runs only
+        if ((((uintptr_t)a.x0 | (uintptr_t)a.x1) & 15) || (batch > 1 && ((size_t)a.in_stride * esz) % 16))
+            a.flags &= ~P2_PREFETCH;
         a.tw = p->d_tw;
         a.tw_cat_top = p->cat_top;
         a.tw_top_tab = p->d_top;
@@ -510,11 +520,7 @@ int exec_common(const sfft_plan *p, const void *x0, const void *x1, void *y0, vo
     if (!workspace) return fail(SFFT_EINVAL, "log2n=%d needs a workspace (sfft_workspace_bytes)", m);
     const int64_t n = int64_t(1) << m;
     const size_t esz = p->dtype == SFFT_F32 ? 4 : 8;
-    // the fused pairs copy their source tiles with 16-byte cp.async: rows that
-    // are not 16-byte aligned take the one-launch-per-group schedule (same groups)
-    const bool rows16 = !(((uintptr_t)x0 | (uintptr_t)x1) & 15) && (batch == 1 || ((size_t)is * esz) % 16 == 0);
-    if (p->fuse2 && !il && rows16)
-        return exec_fused2(p, x0, x1, y0, y1, batch, is, os, inv, scale, workspace, st);
+    if (p->fuse2 && !il) return exec_fused2(p, x0, x1, y0, y1, batch, is, os, inv, scale, workspace, st);
     const int G = (int)p->groups.size();
     char *ws = (char *)workspace;
     const size_t plane = (size_t)batch * (size_t)n * esz;

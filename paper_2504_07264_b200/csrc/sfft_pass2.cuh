@@ -63,9 +63,13 @@ struct Pass2Args {
     const double2 *fine;
 };
 
-// flags: P2_NOPIPE turns the look-ahead load of the next tile off (every tile
-// then loads through its landing buffer at its own start; A/B).
-constexpr int P2_NOPIPE = 1;
+// flags: publish a tile's completion after the NEXT tile's loads are issued
+// (the release fence then waits next to loads every warp waits for, instead
+// of holding warp 0 back at the tile boundary); prefetch the next tile's
+// HBM-side source runs into L2 once its ticket is known (one 128-byte line
+// per thread with prefetch.global.L2; P2_PREFETCH_BULK: cp.async.bulk.prefetch,
+// which the uniform datapath serialises lane by lane -- measured, not used).
+constexpr int P2_DEFER = 1, P2_PREFETCH = 2, P2_PREFETCH_BULK = 4;
 
 template <typename T> struct P2TJ { static constexpr int value = sizeof(T) == 4 ? 32 : 16; };
 
@@ -77,62 +81,14 @@ struct P2Shape {
     static constexpr int NT = TJ * P;
     static constexpr int RS = TJ + 1;
     static constexpr int LMAX = 7;   // p2_tile places the column factors after a 2^7-point tile
-    // landing buffer of one source tile (2^LMAX rows of TJ complex values:
-    // two planes of 128-byte rows, or 256-byte rows of pairs), then the
-    // exchange tile and the column factors
-    static constexpr int LB_PLANE = (1 << LMAX) * TJ * (int)sizeof(T);
-    static constexpr int LB_BYTES = 2 * LB_PLANE;
-    static constexpr int smem_bytes()
-    {
-        return LB_BYTES + (1 << LMAX) * RS * 2 * (int)sizeof(T) + LMAX * TJ * 2 * (int)sizeof(T);
-    }
+    static constexpr int smem_bytes() { return (1 << LMAX) * RS * 2 * (int)sizeof(T) + LMAX * TJ * 2 * (int)sizeof(T); }
 };
 
 template <typename T, int L1, int L2>
 struct P2MinBlocks {
     static constexpr int NT = P2Shape<T, L1, L2>::NT;
-    static constexpr int value = sizeof(T) == 4 ? 3 : 0;   // 66 KiB of shared memory per CTA: three per SM
+    static constexpr int value = sizeof(T) == 4 ? 1024 / NT : 0;
 };
-
-// Asynchronous 16-byte copies global -> shared (L2 only: the block scratch is
-// written by other SMs during the kernel), one commit group per tile.
-__device__ __forceinline__ void p2_cp16(uint32_t dst, const void *src)
-{
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void p2_cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void p2_cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// Issue the copies of one source tile into the landing buffer `lb` (shared
-// address): 2^rows_log rows of TJ complex values at p0 (+ p1: the second
-// plane) with `stride_b` bytes between rows.  pairs: rows of TJ (re, im)
-// pairs (256 bytes) land at lb + 256 e; planes: two 128-byte rows per e land
-// at lb + 128 e and lb + LB_PLANE + 128 e.  16 << rows_log chunks either way.
-template <int NT, int LB_PLANE>
-__device__ __forceinline__ void p2_issue_tile(uint32_t lb, bool pairs, const char *p0, const char *p1,
-                                              uint32_t stride_b, int rows_log, int tid)
-{
-    const int chunks = 16 << rows_log;
-    if (pairs) {
-        const int c = tid & 15;
-        const char *src = p0 + (size_t)(tid >> 4) * stride_b + c * 16;
-        uint32_t dst = lb + (uint32_t)tid * 16u;
-        const size_t step = (size_t)(NT / 16) * stride_b;
-        for (int q = tid; q < chunks; q += NT) {
-            p2_cp16(dst, src);
-            src += step;
-            dst += NT * 16u;
-        }
-    } else {
-        const int per_plane = 8 << rows_log;
-        for (int q = tid; q < chunks; q += NT) {
-            const int pl = q >= per_plane, r = q - pl * per_plane;
-            const char *src = (pl ? p1 : p0) + (size_t)(r >> 3) * stride_b + (r & 7) * 16;
-            p2_cp16(lb + (uint32_t)pl * LB_PLANE + (uint32_t)r * 16u, src);
-        }
-    }
-    p2_cp_commit();
-}
 
 template <typename T, bool S0G>
 __device__ __forceinline__ typename PassTw<T, S0G>::type make_p2_tw(const Pass2Args &a)
@@ -155,33 +111,25 @@ __device__ __forceinline__ typename PassTw<T, S0G>::type make_p2_tw(const Pass2A
 // factor column c0 + jl (S > 0).  Column side: element e of column jl at
 // base + jl + e * stride; row side (the S = 0 group: DIT destination, DIF
 // source): element o of column jl at base + jl * stride + o.
-// Scheduler hooks, each run once per tile: `mid()` after the first register
-// pass (the look-ahead for the next tile, off the tile's critical path),
-// `px()` after the CTA barrier that follows `mid()` (every thread has read
-// its part of the landing buffer by then: the next tile's copies start here).
+// Scheduler hooks, each run once per tile: `ldh()` after the tile's global
+// loads (and column-factor lookups) are issued, `mid()` after the first
+// register pass (the look-ahead for the next tile, off the tile's critical
+// path), `px()` after the CTA barrier that follows `mid()`.
 // The scratch side (IN_SCR: source, OUT_SCR: destination) is `scr`, pairs
 // with the compile-time element stride SSTR; the plane pointers and the
 // runtime stride of that side are unused.
-// USE_LB: the source tile (column side) is in the landing buffer at the
-// start of smem_raw, its copies issued by the caller (p2_issue_tile); the
-// tile waits for them.  Otherwise (the S = 0 DIF group's row-side source) it
-// loads straight from global memory.
-template <typename T, int L, bool DIF, bool S0G, bool IN_SCR, bool OUT_SCR, uint32_t SSTR, bool USE_LB, typename Mid,
-          typename Px>
+template <typename T, int L, bool DIF, bool S0G, bool IN_SCR, bool OUT_SCR, uint32_t SSTR, typename Ldh,
+          typename Mid, typename Px>
 __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr, T *orr, T *oi, uint32_t ostr,
                                         vec2_t<T> *scr, int S, uint32_t c0, const Pass2Args &a,
-                                        unsigned char *smem_raw, const Mid &mid, const Px &px)
+                                        unsigned char *smem_raw, const Ldh &ldh, const Mid &mid, const Px &px)
 {
     constexpr int TJ = P2TJ<T>::value, P = 8, SUB = 1 << L, LR = L - 3, R = 1 << LR, NT = TJ * P;
     constexpr int RS = TJ + 1, NPI = (L + LR - 1) / LR;
     static_assert(L >= 5 && L <= 7, "fused pair groups are 2^5..2^7 points");
     using V = vec2_t<T>;
+    V *sx = reinterpret_cast<V *>(smem_raw);
     constexpr int LMAX = 7;
-    constexpr int LB_PLANE = (1 << LMAX) * TJ * (int)sizeof(T);
-    static_assert(USE_LB || (DIF && S0G), "only the row-side source bypasses the landing buffer");
-    const T *lbp = reinterpret_cast<const T *>(smem_raw);    // planes: [2][row][TJ]
-    const V *lbv = reinterpret_cast<const V *>(smem_raw);    // pairs: [row][TJ]
-    V *sx = reinterpret_cast<V *>(smem_raw + 2 * LB_PLANE);
     V *cs = sx + (1 << LMAX) * RS;   // [L][TJ] column factors (after the largest tile)
     const int tid = threadIdx.x;
     const int jl = tid % TJ, t = tid / TJ;
@@ -191,16 +139,17 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
     const bool scale_out = !OUT_SCR && a.scale_out != 0;   // only the super-group's destination
     const T scale = (T)a.scale;
     constexpr bool CST = FactorTw<T>::value && !S0G;
-    const uint32_t os_b = ostr * (uint32_t)sizeof(T);
+    const uint32_t is_b = istr * (uint32_t)sizeof(T), os_b = ostr * (uint32_t)sizeof(T);
 
-    // source element of row `e` (landing buffer: rows of TJ values, this thread's column jl)
-    auto get_row = [&](uint32_t e) {
+    // source element at `k` strides / `off` elements from the thread's base
+    // (planes pr, pi or scratch pairs ps); destination likewise
+    auto get_k = [&](const T *pr, const T *pi, const V *ps, uint32_t k) {
         V w;
         if constexpr (IN_SCR) {
-            w = lbv[e * TJ + jl];
+            w = __ldcg(ps + k * SSTR);   // written by other SMs during this kernel: L2, never L1
         } else {
-            w.x = lbp[e * TJ + jl];
-            w.y = lbp[LB_PLANE / (int)sizeof(T) + e * TJ + jl];
+            w.x = ld_stream(at_stride(pr, is_b, k));
+            w.y = ld_stream(at_stride(pi, is_b, k));
         }
         return w;
     };
@@ -226,9 +175,11 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
                 const int st = k / TJ, l = k - st * TJ;
                 cs[k] = tw.get(S + 1 + st, (I)(c0 + (uint32_t)l));
             }
+            ldh();
+            __syncthreads();
+        } else {
+            ldh();
         }
-        if constexpr (USE_LB) p2_cp_wait_all();          // this thread's copies of the source tile
-        if constexpr (USE_LB || CST) __syncthreads();    // everyone's copies and the column factors
     };
     auto column_factors = [&](int sp, int KP, int jp, V *cf) {
         const int x = jp & ((1 << sp) - 1);
@@ -248,11 +199,13 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
     V v[R];
     if constexpr (!DIF) {
         // column-side source: element (t + k) of column jl
+        const T *in_r = IN_SCR ? nullptr : ir + jl + (size_t)t * istr;
+        const T *in_i = IN_SCR ? nullptr : ii + jl + (size_t)t * istr;
+        const V *in_s = IN_SCR ? scr + jl + t * SSTR : nullptr;
         static_for<0, NPI>([&](auto PPC) {
             constexpr int pp = decltype(PPC)::value;
             constexpr int sp = pp * LR, KP = cmin(LR, L - sp), RP = 1 << KP, U = R / RP, nsp = 1 << sp;
             constexpr bool last = pp == NPI - 1;
-            if constexpr (pp == 0) stage_columns();
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int jp = t + P * u;
@@ -260,12 +213,13 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
                 for (int r = 0; r < RP; ++r) {
                     if constexpr (pp == 0) {
                         const uint32_t k = (uint32_t)(P * u + r * (SUB / RP));
-                        v[u * RP + r] = get_row((uint32_t)t + k);
+                        v[u * RP + r] = get_k(in_r, in_i, in_s, k);
                     } else {
                         v[u * RP + r] = sx[(jp + r * (SUB / RP)) * RS + jl];
                     }
                 }
             }
+            if constexpr (pp == 0) stage_columns();
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int jp = t + P * u;
@@ -327,6 +281,7 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
                     v[kk].y = ld_stream(ii + off);
                 }
             }
+            ldh();
 #pragma unroll
             for (int kk = 0; kk < R; ++kk) {
                 const int k = tid + kk * NT, jj = k >> L, o = k & (SUB - 1);
@@ -334,11 +289,12 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
             }
             __syncthreads();
         }
+        const T *in_r = IN_SCR ? nullptr : ir + jl, *in_i = IN_SCR ? nullptr : ii + jl;
+        const V *in_s = IN_SCR ? scr + jl : nullptr;
         static_for<0, NPI>([&](auto QC) {
             constexpr int pp = NPI - 1 - decltype(QC)::value;
             constexpr int sp = pp * LR, KP = cmin(LR, L - sp), RP = 1 << KP, U = R / RP, nsp = 1 << sp;
             constexpr bool first = pp == NPI - 1;
-            if constexpr (first && !S0G) stage_columns();
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int jp = t + P * u;
@@ -347,12 +303,19 @@ __device__ __forceinline__ void p2_tile(const T *ir, const T *ii, uint32_t istr,
                 for (int f = 0; f < RP; ++f) {
                     const int d = u * RP + brev(f, KP);
                     if constexpr (first && !S0G) {
-                        v[d] = get_row((uint32_t)(base + nsp * f));
+                        const uint32_t k = (uint32_t)(nsp * f);
+                        if constexpr (IN_SCR) {
+                            v[d] = get_k(nullptr, nullptr, in_s + (uint32_t)base * SSTR, k);
+                        } else {
+                            const T *pr = in_r + (size_t)base * istr, *pi = in_i + (size_t)base * istr;
+                            v[d] = get_k(pr, pi, nullptr, k);
+                        }
                     } else {
                         v[d] = sx[(base + nsp * f) * RS + jl];
                     }
                 }
             }
+            if constexpr (first && !S0G) stage_columns();
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int jp = t + P * u;
@@ -403,6 +366,12 @@ __device__ __forceinline__ unsigned p2_ld_relaxed(const unsigned *p)
 __device__ __forceinline__ void p2_signal(unsigned *p)
 {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+
+// L2 prefetch of one contiguous run (no destination, nothing to wait for)
+__device__ __forceinline__ void p2_prefetch_run(const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
 // One scheduled tile: phase (0: the group run first), block, tile index, and
@@ -492,13 +461,9 @@ sfft_pass2_kernel(const Pass2Args a)
     };
 
     __shared__ int s_ok[2];
-    // the next tile's source, written by thread 0 in mid(): kind 0 none
-    // (not loaded ahead), 1 planes (the super-group's source), 2 scratch pairs
-    __shared__ const char *s_src[2];
-    __shared__ uint32_t s_src_stride;
-    __shared__ int s_src_kind, s_src_rows_log;
-    const uint32_t lb = (uint32_t)__cvta_generic_to_shared(smem_raw);
-    constexpr int LBP = Sh::LB_PLANE;
+    __shared__ const char *s_pf[2];    // the next tile's HBM-side source runs (P2_PREFETCH)
+    __shared__ uint32_t s_pf_stride;
+    __shared__ int s_pf_rows;
 
     // the two groups' tile geometry (see the comment above the kernel)
     struct Geom {
@@ -532,102 +497,80 @@ sfft_pass2_kernel(const Pass2Args a)
         }
         return g;
     };
-    // compile-time scratch strides of the two groups (pairs)
-    constexpr uint32_t SS1 = SZ ? (1u << L) : (uint32_t)TJ;
-    constexpr uint32_t SS2 = SZ ? (1u << L1) : ((uint32_t)TJ << L1);
-    // the source tile of scheduled item q as the landing-buffer copies see it;
-    // kind 0: the S = 0 DIF group's row-side source (loaded by the tile itself)
-    struct Src {
-        const char *p0, *p1;
-        uint32_t stride;
-        int kind, rows_log;
-    };
-    auto source = [&](const P2Item &q) {
-        Src r;
-        const int64_t row = q.b >> (m - L - LTJ);
-        const uint32_t J0 = ((uint32_t)q.b & (nbr - 1u)) * TJ;
-        const bool fg = (q.ph == 0) != DIF;
-        const Geom g = geom(fg, (uint32_t)q.tile, J0);
-        r.rows_log = fg ? L1 : L2;
-        if (q.ph == 0) {   // the super-group's source planes
-            r.kind = 1;
-            r.p0 = (const char *)((const T *)a.x0 + row * a.in_stride + g.xo);
-            r.p1 = (const char *)((const T *)a.x1 + row * a.in_stride + g.xo);
-            r.stride = g.xs * (uint32_t)sizeof(T);
-        } else {           // the block scratch
-            r.kind = (DIF && SZ) ? 0 : 2;
-            r.p0 = (const char *)((const vec2_t<T> *)a.s0 + q.slot * slot_elems + g.so);
-            r.p1 = nullptr;
-            r.stride = (fg ? SS1 : SS2) * 2u * (uint32_t)sizeof(T);
-        }
-        return r;
-    };
 
-    // tickets are taken two tiles ahead: s_item[it & 1] is this tile's,
-    // s_item[(it + 1) & 1] the next one's (its dependency is polled at the top
-    // of this tile and its source loaded ahead from px()), and the ticket
-    // after that is requested at the top and stored at the end of this tile
+    int pend = 0;   // thread 0: index in ctr[] of a finished tile's counter, not yet published (P2_DEFER)
+    auto flush = [&]() {
+        if (pend) {
+            p2_signal(a.ctr + pend);
+            pend = 0;
+        }
+    };
     if (tid == 0) {
         s_item[0] = atomicAdd(a.ctr, 1u);
-        s_item[1] = atomicAdd(a.ctr, 1u);
         s_ok[0] = 0;
-        s_src_kind = 0;
     }
     __syncthreads();
     for (int it = 0;; ++it) {
         const uint32_t g = s_item[it & 1];
-        if (g >= total) return;
-        const bool ok = s_ok[it & 1] != 0;
-        const bool loaded = s_src_kind != 0;   // this tile's source copies are in flight (or landed)
-        const P2Item q = decode(g);
-        unsigned nn = 0, polled = 0, want = 0;
-        bool nodep = true;
-        if (tid == 0) {
-            nn = atomicAdd(a.ctr, 1u);
-            const uint32_t gn = s_item[(it + 1) & 1];
-            if (gn < total) {
-                const P2Item n = decode(gn);
-                nodep = n.dep == nullptr;
-                if (!nodep) {
-                    polled = p2_ld_relaxed(n.dep);   // consumed in mid()
-                    want = n.target;
-                }
-            }
-            if (!ok && q.dep)   // the look-ahead poll did not see this tile's dependency satisfied
-                while (p2_ld_relaxed(q.dep) < q.target) __nanosleep(64);
+        if (g >= total) {
+            if (tid == 0) flush();
+            return;
         }
-        if (!ok) __syncthreads();
-        const Src cur = source(q);
-        if (!loaded && cur.kind != 0)
-            p2_issue_tile<Sh::NT, LBP>(lb, cur.kind == 2, cur.p0, cur.p1, cur.stride, cur.rows_log, tid);
-
-        // look-ahead: is the next tile's dependency satisfied?  If so (or if it
-        // reads the super-group's source, which nothing writes), describe its
-        // source for px()
+        const bool ok = s_ok[it & 1] != 0;
+        const P2Item q = decode(g);
+        // the next ticket: issued now, consumed after the first register pass
+        unsigned nxt = 0;
+        if (tid == 0) nxt = atomicAdd(a.ctr, 1u);
+        if (!ok) {   // the look-ahead poll did not see the dependency satisfied
+            if (tid == 0) {
+                flush();   // what this CTA still owes may be what it is about to wait for
+                if (q.dep)
+                    while (p2_ld_relaxed(q.dep) < q.target) __nanosleep(64);
+            }
+            __syncthreads();
+        }
+        auto ldh = [&]() {
+            if (tid == 0) flush();
+        };
+        // look-ahead: decode the next ticket and poll its dependency once;
+        // the poll's value is only needed at the end of this tile
+        unsigned polled = 0, want = 0;
+        bool nodep = true;
         auto mid = [&]() {
             if (tid == 0) {
-                int kind = 0;
-                const bool okn = nodep || polled >= want;
-                const uint32_t gn = s_item[(it + 1) & 1];
-                if (gn < total && !(a.flags & P2_NOPIPE)) {
-                    const P2Item n = decode(gn);
-                    if (n.ph == 0 || okn) {
-                        const Src sn = source(n);
-                        kind = sn.kind;
-                        s_src[0] = sn.p0;
-                        s_src[1] = sn.p1;
-                        s_src_stride = sn.stride;
-                        s_src_rows_log = sn.rows_log;
+                int pf_rows = 0;
+                if (nxt < total) {
+                    const P2Item n = decode(nxt);
+                    nodep = n.dep == nullptr;
+                    if (!nodep) {
+                        polled = p2_ld_relaxed(n.dep);
+                        want = n.target;
+                    }
+                    if ((a.flags & P2_PREFETCH) && n.ph == 0) {   // phase 0 reads the super-group's source planes
+                        const int64_t nrow = n.b >> (m - L - LTJ);
+                        const uint32_t nJ0 = ((uint32_t)n.b & (nbr - 1u)) * TJ;
+                        const Geom ng = geom(!DIF, (uint32_t)n.tile, nJ0);
+                        s_pf[0] = (const char *)((const T *)a.x0 + nrow * a.in_stride + ng.xo);
+                        s_pf[1] = (const char *)((const T *)a.x1 + nrow * a.in_stride + ng.xo);
+                        s_pf_stride = ng.xs * (uint32_t)sizeof(T);
+                        pf_rows = 1 << (DIF ? L2 : L1);
                     }
                 }
-                s_src_kind = kind;
-                s_ok[(it + 1) & 1] = okn;
+                if (a.flags & P2_PREFETCH) s_pf_rows = pf_rows;
             }
         };
         auto px = [&]() {
-            const int kind = s_src_kind;
-            if (kind != 0)
-                p2_issue_tile<Sh::NT, LBP>(lb, kind == 2, s_src[0], s_src[1], s_src_stride, s_src_rows_log, tid);
+            if (a.flags & P2_PREFETCH) {
+                const int rows = s_pf_rows;
+                for (int k = tid; k < 2 * rows; k += Sh::NT) {
+                    const int pl = k >= rows, e = k - pl * rows;
+                    const char *run = s_pf[pl] + (size_t)e * s_pf_stride;   // one 128-byte line
+                    if (a.flags & P2_PREFETCH_BULK)
+                        p2_prefetch_run(run, TJ * (uint32_t)sizeof(T));
+                    else
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(run) : "memory");
+                }
+            }
         };
 
         const int64_t row = q.b >> (m - L - LTJ);
@@ -635,28 +578,42 @@ sfft_pass2_kernel(const Pass2Args a)
         vec2_t<T> *sc = (vec2_t<T> *)a.s0 + q.slot * slot_elems;
         const bool first_group = (q.ph == 0) != DIF;   // group (S, L1)?
         const Geom gm = geom(first_group, (uint32_t)q.tile, J0);
+        // compile-time scratch strides of the two groups (see geom: g.ss)
+        constexpr uint32_t SS1 = SZ ? (1u << L) : (uint32_t)TJ;
+        constexpr uint32_t SS2 = SZ ? (1u << L1) : ((uint32_t)TJ << L1);
         if (first_group) {
             if constexpr (!DIF) {
-                p2_tile<T, L1, false, SZ, false, true, SS1, true>(nullptr, nullptr, 0u, nullptr, nullptr, 0u, sc + gm.so,
-                                                                  S, gm.cc, a, smem_raw, mid, px);
+                const T *xr = (const T *)a.x0 + row * a.in_stride + gm.xo, *xi = (const T *)a.x1 + row * a.in_stride + gm.xo;
+                p2_tile<T, L1, false, SZ, false, true, SS1>(xr, xi, gm.xs, nullptr, nullptr, 0u, sc + gm.so, S, gm.cc,
+                                                            a, smem_raw, ldh, mid, px);
             } else {
                 T *yr = (T *)a.y0 + row * a.out_stride + gm.xo, *yi = (T *)a.y1 + row * a.out_stride + gm.xo;
-                p2_tile<T, L1, true, SZ, true, false, SS1, !SZ>(nullptr, nullptr, 0u, yr, yi, gm.xs, sc + gm.so, S,
-                                                                gm.cc, a, smem_raw, mid, px);
+                p2_tile<T, L1, true, SZ, true, false, SS1>(nullptr, nullptr, 0u, yr, yi, gm.xs, sc + gm.so, S, gm.cc,
+                                                           a, smem_raw, ldh, mid, px);
             }
         } else {
             if constexpr (!DIF) {
                 T *yr = (T *)a.y0 + row * a.out_stride + gm.xo, *yi = (T *)a.y1 + row * a.out_stride + gm.xo;
-                p2_tile<T, L2, false, false, true, false, SS2, true>(nullptr, nullptr, 0u, yr, yi, gm.xs, sc + gm.so,
-                                                                     S + L1, gm.cc, a, smem_raw, mid, px);
+                p2_tile<T, L2, false, false, true, false, SS2>(nullptr, nullptr, 0u, yr, yi, gm.xs, sc + gm.so, S + L1,
+                                                               gm.cc, a, smem_raw, ldh, mid, px);
             } else {
-                p2_tile<T, L2, true, false, false, true, SS2, true>(nullptr, nullptr, 0u, nullptr, nullptr, 0u,
-                                                                    sc + gm.so, S + L1, gm.cc, a, smem_raw, mid, px);
+                const T *xr = (const T *)a.x0 + row * a.in_stride + gm.xo, *xi = (const T *)a.x1 + row * a.in_stride + gm.xo;
+                p2_tile<T, L2, true, false, false, true, SS2>(xr, xi, gm.xs, nullptr, nullptr, 0u, sc + gm.so, S + L1,
+                                                              gm.cc, a, smem_raw, ldh, mid, px);
             }
         }
-        if (tid == 0) s_item[it & 1] = nn;   // the ticket of tile it + 2
+        if (tid == 0) {
+            s_item[(it + 1) & 1] = nxt;
+            s_ok[(it + 1) & 1] = nodep || polled >= want;
+        }
         __syncthreads();   // every thread's stores of this tile issued; shared reads done
-        if (tid == 0) p2_signal(a.ctr + 1 + (q.ph == 0 ? 0 : nslot) + q.slot);   // doneA / doneB
+        if (tid == 0) {
+            const int c = 1 + (q.ph == 0 ? 0 : nslot) + q.slot;   // doneA / doneB
+            if (a.flags & P2_DEFER)
+                pend = c;   // published by flush(): after the next tile's loads, or before a wait / the exit
+            else
+                p2_signal(a.ctr + c);
+        }
     }
 }
 
