@@ -54,8 +54,8 @@ extern "C" {
 #define SFFT_KERNEL_AUTO 0  /* TMA-fed persistent kernel when the rows allow it, else LDG/STG */
 #define SFFT_KERNEL_LDG 1   /* per-thread global loads/stores (any stride/alignment, interleaved) */
 #define SFFT_KERNEL_TMA 2   /* require the TMA kernel (planar, 16-byte aligned rows and strides) */
-#define SFFT_KERNEL_PASS 3  /* log2n > 12: one launch per stage group (required; auto picks PASS2 where it applies) */
-#define SFFT_KERNEL_PASS2 4 /* 20 <= log2n <= 28: L2-fused group pairs, two launches (auto's choice there) */
+#define SFFT_KERNEL_PASS 3  /* log2n > 12: one launch per stage group (auto's choice except fp64 log2n = 28) */
+#define SFFT_KERNEL_PASS2 4 /* 20 <= log2n <= 28: L2-fused group pairs, two launches (auto: fp64 log2n = 28 only) */
 
 /* plan limit, transform.py:32 (MAX_PLAN_M) */
 #define SFFT_MAX_LOG2N 30
