@@ -88,3 +88,27 @@ def check(status: int) -> None:
 
 def launch_count() -> int:
     return int(lib.sfft_launch_count())
+
+
+# Optional NVTX ranges around the exec calls and the sharded phases
+# (SFFT_NVTX=1; off by default: a range push/pop costs a few microseconds per
+# exec, comparable to a small launch).  Timelines: nsys / ncu --nvtx.
+NVTX = os.environ.get("SFFT_NVTX", "0") == "1"
+
+
+class nvtx_range:
+    """``with nvtx_range("name"):`` -- a no-op unless SFFT_NVTX=1."""
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        if NVTX:
+            import torch
+            torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *exc):
+        if NVTX:
+            import torch
+            torch.cuda.nvtx.range_pop()
+        return False

@@ -181,10 +181,12 @@ class P2PExchange:
 
     def run(self, x_re, x_im, y_re, y_im, inverse=False, workspace=None):
         self.handle.barrier(channel=0)          # every rank done reading its receive planes
-        self.plan.phase0_p2p(x_re, x_im, self.peer_re, self.peer_im, inverse=inverse, workspace=workspace)
+        with _ffi.nvtx_range("sfft_dist_phase0_p2p"):
+            self.plan.phase0_p2p(x_re, x_im, self.peer_re, self.peer_im, inverse=inverse, workspace=workspace)
         self.handle.barrier(channel=0)          # every store landed
-        return self.plan.phase(1, self.recv_re, self.recv_im, y_re, y_im, inverse=inverse,
-                               workspace=workspace)
+        with _ffi.nvtx_range("sfft_dist_phase1"):
+            return self.plan.phase(1, self.recv_re, self.recv_im, y_re, y_im, inverse=inverse,
+                                   workspace=workspace)
 
 
 def scatter_input(x, world, rank, l1):
@@ -210,7 +212,8 @@ def exchange(send, recv, group=None):
     """The all-to-all of one plane: segment r of this rank's send buffer goes
     to slot (this rank) of rank r's receive buffer."""
     import torch.distributed as dist
-    dist.all_to_all_single(recv, send, group=group)
+    with _ffi.nvtx_range("sfft_dist_all_to_all"):
+        dist.all_to_all_single(recv, send, group=group)
     return recv
 
 

@@ -229,9 +229,10 @@ def _exec_split_device(plan, xr, xi, yr, yi, inverse):
     _, ostr = _rows(yr)
     ws, wsp = _workspace(plan, batch)
     direction = _ffi.SFFT_INVERSE if inverse else _ffi.SFFT_FORWARD
-    _ffi.check(_ffi.lib.sfft_exec_split(plan._handle, xr.data_ptr(), xi.data_ptr(), yr.data_ptr(),
-                                        yi.data_ptr(), batch, istr, ostr, direction, wsp,
-                                        _stream_ptr(plan.device)))
+    with _ffi.nvtx_range("sfft_exec_split"):
+        _ffi.check(_ffi.lib.sfft_exec_split(plan._handle, xr.data_ptr(), xi.data_ptr(), yr.data_ptr(),
+                                            yi.data_ptr(), batch, istr, ostr, direction, wsp,
+                                            _stream_ptr(plan.device)))
     if ws is not None:
         ws.record_stream(torch.cuda.current_stream(plan.device))
 
