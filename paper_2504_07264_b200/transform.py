@@ -173,8 +173,8 @@ def make_plan(m: int, algorithm=Algorithm.DIT, *, max_m: int = MAX_PLAN_M,
     overrides the register radix of the fused kernel (0 = tuned default);
     ``kernel`` picks the fused kernel family: "auto" (TMA-fed when the rows
     allow it), "ldg" (per-thread loads) or "tma" (required); for m > 12
-    "pass" forces one launch per stage group and "pass2" the L2-fused group
-    pairs (auto's choice for 20 <= m <= 28, planar rows);
+    "pass" forces one launch per stage group and "pass2" (20 <= m <= 28,
+    planar rows) the L2-fused group pairs (auto takes them for fp64 m = 28);
     ``prefetch_factors`` (fp32) forces fetching each pass's base factors
     before the data on/off (None = tuned default).
     """
