@@ -52,7 +52,7 @@ import workloads  # noqa: E402
 
 BASELINE_METRIC = "batched split-DFT transforms/s and achieved HBM GB/s vs peak at 1/2/4/8 B200"
 FALLBACK_HBM_GBS = 6650.0
-SPINUP_S = 0.3   # extra untimed warm-up time after the W warm-up steps (clock ramp)
+SPINUP_S = 0.5   # extra untimed warm-up time after the W warm-up steps (power/clock state settles)
 
 
 def parse():
@@ -417,25 +417,30 @@ def run_ours(args):
                                             y_re.data_ptr(), y_im.data_ptr(), b, n, n,
                                             _ffi.SFFT_FORWARD, ws.data_ptr() if ws_bytes else None, sp))
 
+    # The clock sampler and the events exist before the warm-up so that nothing
+    # but a synchronize (and the rank barrier) sits between the last warm-up
+    # step and the timed region: an idle gap of even ~20 ms lets the power
+    # controller re-boost the SM clock, and the first ~100 ms after that run
+    # 5-9% slower than the settled state while it pulls the clock back under
+    # the power cap (tools/spread_probe.py, profiles/r02aj_spread_probe.txt:
+    # 1.47 -> 1.34 ms per step over 150 back-to-back steps of the headline).
+    clocks = ClockSampler(device)
+    clocks.start()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize(device)
-    # the W warm-up steps of a short step leave an idle GPU at low clocks;
-    # keep stepping (untimed) until the clocks have ramped (>= SPINUP_S)
+    # the W warm-up steps of a short step are over before the clocks settle:
+    # keep stepping (untimed) for SPINUP_S, then go straight into the timed steps
     spin0 = time.perf_counter()
     while time.perf_counter() - spin0 < SPINUP_S:
         for _ in range(20):
             step()
         torch.cuda.synchronize(device)
-
-    clocks = ClockSampler(device)
-    clocks.start()
-    time.sleep(0.02)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(device)
     launches0 = _ffi.launch_count()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     # one event pair around the K steps: nothing sits between consecutive
     # launches of the stream (per-step events cost ~2% on the 0.17 ms cfg2
     # step and block the TMA kernel's dependent launch); SFFT_BENCH_STEP_EVENTS=1
