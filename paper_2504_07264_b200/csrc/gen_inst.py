@@ -71,10 +71,14 @@ TMA_CONFIGS = {
 # warp-per-signal bulk-copy kernel (sfft_tma_warp.cuh, N = 1024, radix 32):
 # (warps per CTA, second-pass factor stages held in registers, factors in
 # tensor memory instead, shared slot ring, ring slots beyond one per warp);
-# selected as the TMA family's radix 2^5 for these sizes.  9 warps sharing a
-# ring of 11 slots (176 KiB): +3-5% over 7 warps with two slots each
-# (profiles/r02p_ab_slot_ring.txt, r02q_ab_ring_depth.txt)
-TMAW_CONFIGS = {"f64": {10: (9, 3, 1, 1, 2, 1)}, "f32": {12: (8, 0, 0, 1, 2, 2)}}
+# selected as the TMA family's radix 2^5 for these sizes.  10 warps sharing a
+# ring of 12 slots (192 KiB).  Timed right after an idle gap (boosted 1.9 GHz
+# SM clock) 9 warps + 11 slots measured best (profiles/r02p_ab_slot_ring.txt,
+# r02q_ab_ring_depth.txt); in the settled power state (1.4-1.5 GHz under the
+# 1000 W cap, the state bench.py times since r02al) the tenth warp is worth
+# 3-4%: 1.370 vs 1.421 ms DIT, 1.379 vs 1.420 ms DIF, 11 / 12 warps, an
+# L2 prefetch-ahead and a 13-slot ring all slower (profiles/r02ao_*, r02ap_*)
+TMAW_CONFIGS = {"f64": {10: (10, 3, 1, 1, 2, 1)}, "f32": {12: (8, 0, 0, 1, 2, 2)}}
 # fp32 N = 4096: two warps per signal, radix 64, 8 warps / 6 slots per SM,
 # factors formed from per-thread base factors (TMEM factors measured no
 # better for fp32: profiles/r02u_ab_cfg4_group_kernel_tmem.txt); +2% over the
