@@ -438,6 +438,15 @@ def run_ours(args):
             step()
         torch.cuda.synchronize(device)
     if world > 1:
+        # the ranks leave their spin-up up to one burst apart: align them, settle
+        # again together for 0.1 s (short bursts), and align once more -- the
+        # second barrier then idles nobody for longer than a few steps
+        dist.barrier()
+        spin0 = time.perf_counter()
+        while time.perf_counter() - spin0 < 0.1:
+            for _ in range(5):
+                step()
+            torch.cuda.synchronize(device)
         dist.barrier()
     torch.cuda.synchronize(device)
     launches0 = _ffi.launch_count()
